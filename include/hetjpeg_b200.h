@@ -1,0 +1,179 @@
+/*
+ * hetjpeg_b200.h - C ABI of the B200-native "parallel phase" of the hetjpeg
+ * JPEG decoder (dequantise -> IDCT -> chroma upsample -> YCbCr->RGB) and of
+ * its host entropy stage.
+ *
+ * Plain pointers and sizes only; no CUDA or torch types.  Every function
+ * returns an hj_status (0 = OK); hj_last_error() gives the message of the
+ * calling thread's last failure.  Streams are passed as `void*` holding a
+ * cudaStream_t (NULL = the library's per-thread default stream).
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to the reference root, pkg/src/hetjpeg/...).
+ */
+#ifndef HETJPEG_B200_H
+#define HETJPEG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  1..4 mirror the native decoder's ERR_* enum
+ * (kernels/_native.pyx:18-23); the host wrapper maps them onto the
+ * reference exception classes (errors.py:4-69). */
+typedef enum {
+    HJ_OK = 0,
+    HJ_ERR_EXHAUSTED = 1,   /* BitstreamExhausted */
+    HJ_ERR_BADCODE = 2,     /* BadCode */
+    HJ_ERR_MARKER = 3,      /* MarkerInScan (non-restart marker) */
+    HJ_ERR_RST_SEQ = 4,     /* MarkerInScan (restart out of sequence) */
+    HJ_ERR_ARG = 16,        /* invalid argument (ValueError) */
+    HJ_ERR_CUDA = 17,       /* CUDA runtime failure */
+    HJ_ERR_NOMEM = 18,      /* allocation failure */
+    HJ_ERR_NODEVICE = 19    /* no CUDA device visible */
+} hj_status;
+
+/* Chroma subsampling of a frame.  420 is this library's documented
+ * extension: the reference accepts only 4:4:4 and 4:2:2
+ * (parser.py:223-229); see DESIGN.md "4:2:0 extension". */
+enum { HJ_SUB_444 = 0, HJ_SUB_422 = 1, HJ_SUB_420 = 2 };
+
+/* Flags for hj_image_t.flags */
+enum { HJ_FLAG_DIRECT_IDCT = 1 };   /* idct="direct" (cli.py:249); default AAN "fast" */
+
+/* One image (or an MCU-row range of one) for the device-resident batch API.
+ * All pointers are DEVICE pointers.  Layout of the coefficient planes is the
+ * reference CoefficientBuffer (entropy.py:31-56): int16 [n_blocks][64],
+ * natural (de-zigzagged) order, Y blocks MCU-ordered (ypm = 1/2/4 per MCU).
+ * q is the (3,64) int32 de-zigzagged qtable stack (perf_model.py:306-311).
+ * rgb is (height, width, 3) uint8, row-major (block_transforms.py:45-57). */
+typedef struct {
+    const int16_t *y;
+    const int16_t *cb;
+    const int16_t *cr;
+    const int32_t *q;
+    uint8_t *rgb;
+    int32_t width, height;
+    int32_t mcus_per_row, mcu_rows;
+    int32_t row0, n_rows;   /* MCU rows to render: [row0, row0+n_rows) */
+    int32_t subsampling;    /* HJ_SUB_* */
+    int32_t flags;          /* HJ_FLAG_* */
+} hj_image_t;
+
+/* ---- library / device ------------------------------------------------ */
+const char *hj_version(void);
+const char *hj_last_error(void);
+int hj_device_count(void);
+hj_status hj_set_device(int device);
+
+/* Device / pinned-host memory and copies, so hosts need no other CUDA binding. */
+hj_status hj_malloc_device(void **ptr, size_t bytes);
+hj_status hj_free_device(void *ptr);
+hj_status hj_malloc_host(void **ptr, size_t bytes);     /* page-locked */
+hj_status hj_free_host(void *ptr);
+hj_status hj_memcpy_h2d(void *dst, const void *src, size_t bytes, void *stream);
+hj_status hj_memcpy_d2h(void *dst, const void *src, size_t bytes, void *stream);
+hj_status hj_memset_device(void *dst, int value, size_t bytes, void *stream);
+hj_status hj_stream_create(void **stream);
+hj_status hj_stream_destroy(void *stream);
+hj_status hj_stream_synchronize(void *stream);
+hj_status hj_device_synchronize(void);
+
+/* Events for device-side timing on a given stream. */
+hj_status hj_event_create(void **event);
+hj_status hj_event_destroy(void *event);
+hj_status hj_event_record(void *event, void *stream);
+hj_status hj_event_elapsed_ms(void *start, void *end, float *ms);
+
+/* ---- the parallel phase: device-resident batch ---------------------- */
+/* Render every image of the batch on `stream` (asynchronous).  Replaces the
+ * per-lane render_rows dispatch (block_transforms.py:60-75 ->
+ * kernels/_native.pyx:493-549) with one launch per subsampling present.
+ * Output rows [8*row0*vs, min(h, 8*vs*(row0+n_rows))) are written (vs = 2 for
+ * 4:2:0, else 1); nothing else.  4:2:0 reads the chroma blocks of MCU rows
+ * row0-1 and row0+n_rows when they exist (the vertical filter's context). */
+hj_status hj_render_batch(const hj_image_t *images, int n_images, void *stream);
+
+/* Reusable launch plan for a fixed batch (tile list resident on the device;
+ * what a CUDA graph or a steady-state pipeline replays).  The hj_image_t
+ * array is copied at creation: pointers inside it must stay valid. */
+hj_status hj_plan_create(const hj_image_t *images, int n_images, void **plan);
+hj_status hj_plan_launch(void *plan, void *stream);
+hj_status hj_plan_destroy(void *plan);
+
+/* Number of kernel launches hj_render_batch issued since library load
+ * (evidence for the bench's gpu_launches claim). */
+uint64_t hj_launch_count(void);
+
+/* ---- the parallel phase: synchronous host-buffer drop-in -------------- */
+/* Exactly the backend contract of render_rows_444 / render_rows_422
+ * (kernels/_native.pyx:532-549, kernels/fallback.py:224-260): HOST arrays,
+ * blocks of the whole image, rgb (height, width, 3) written in place for the
+ * MCU rows [row0, row0+n_rows); returns after the RGB rows are in `rgb`.
+ * `fast` selects the AAN (1) or direct-basis (0) transform; `fused` is
+ * accepted for interface parity and never changes bytes.  y/cb/cr must hold
+ * every block of the image (n_y_blocks / n_c_blocks give their counts, used
+ * for bounds checks).  Re-entrant: each host thread uses its own stream and
+ * staging buffers. */
+hj_status hj_render_rows(const int16_t *y, const int16_t *cb, const int16_t *cr,
+                         const int32_t *q3x64, uint8_t *rgb,
+                         int32_t width, int32_t height, int32_t mcus_per_row,
+                         int32_t mcu_rows, int32_t row0, int32_t n_rows,
+                         int32_t subsampling, int32_t fast, int32_t fused,
+                         int64_t n_y_blocks, int64_t n_c_blocks);
+
+/* Single-block transforms for the reference's per-block API
+ * (block_transforms.py / fallback.py:103-119): n dequantised blocks
+ * (int32, natural order) -> 64 samples each (uint8, +128, rounded, clamped),
+ * or the float64 pre-rounding core.  HOST buffers, synchronous. */
+hj_status hj_idct_blocks(const int32_t *deq, int64_t n, uint8_t *out, int32_t fast);
+hj_status hj_idct_blocks_f64(const int32_t *deq, int64_t n, double *out, int32_t fast);
+/* Algorithm 1 single-row 4:2:2 upsample (fallback.py:122-139):
+ * n rows of 8 chroma samples -> 16 int32 each; left/right[i] < 0 means "no
+ * neighbour" (end pixel copied).  HOST buffers, synchronous. */
+hj_status hj_upsample_422(const uint8_t *rows, const int16_t *left, const int16_t *right,
+                          int32_t *out, int64_t n);
+/* Colour conversion of n sample triples (fallback.py:142-150). HOST buffers. */
+hj_status hj_ycbcr_to_rgb(const uint8_t *y, const uint8_t *cb, const uint8_t *cr,
+                          uint8_t *rgb, int64_t n);
+
+/* ---- host entropy stage (CPU, C++) ------------------------------------ */
+/* Packed scan tables, the arrays entropy._pack_scan_tables builds
+ * (entropy.py:59-84): 8 slots (0-3 DC, 4-7 AC). */
+typedef struct {
+    uint8_t lut_sym[8][256];
+    uint8_t lut_len[8][256];
+    int32_t mincode[8][17];
+    int32_t maxcode[8][17];
+    int32_t valptr[8][17];
+    uint8_t symbols[8][256];
+    int32_t comp_dc[3];
+    int32_t comp_ac[3];
+} hj_scan_tables_t;
+
+/* Huffman-decode MCU rows [row0, row0+n_rows) into the coefficient planes
+ * (HOST buffers).  Replaces decode_mcu_rows (kernels/_native.pyx:195-305,
+ * fallback.py:282-417): identical bit reader, lookahead + maxcode walk,
+ * EXTEND, EOB/ZRL, restart handling and int64[8] resumable state
+ * {pos, bitbuf, bits, mcus_since_rst, next_rst, predY, predCb, predCr}.
+ * On error the state is still written back (native behaviour) and the
+ * HJ_ERR_* code returned. */
+hj_status hj_decode_mcu_rows(const uint8_t *data, int64_t n_bytes, int64_t *state,
+                             const hj_scan_tables_t *scan,
+                             int16_t *y_out, int16_t *cb_out, int16_t *cr_out,
+                             int32_t row0, int32_t n_rows, int32_t mcus_per_row,
+                             int32_t y_per_mcu, int32_t restart_interval);
+
+/* Index of the first non-restart marker after the scan data starting at
+ * `start`, or -1 if the stream ends inside the entropy-coded data
+ * (parser.py:277-293, _scan_entropy_end). */
+int64_t hj_scan_entropy_end(const uint8_t *data, int64_t n_bytes, int64_t start);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HETJPEG_B200_H */

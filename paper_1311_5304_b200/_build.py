@@ -1,0 +1,61 @@
+"""Build the native library in-tree: nvcc for sm_100a, no JIT, no torch.
+
+    python -m paper_1311_5304_b200._build          # library only
+    python -m paper_1311_5304_b200._build --all    # + the CPU oracle (tests only)
+
+Output: paper_1311_5304_b200/libhetjpeg_b200.so (git-ignored, travels with
+gpurun snapshots).  Rebuilds only when a source is newer than the library.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libhetjpeg_b200.so")
+SOURCES = ["hj_render.cu", "hj_api.cu", "hj_entropy.cpp"]
+HEADERS = ["hj_render.cuh", "hj_tables.h", os.path.join("..", "..", "include", "hetjpeg_b200.h")]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
+         "-Xptxas", "-warn-spills"]
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_library(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    if verbose:
+        print(" ".join(cmd))
+    res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+def build_oracle() -> str:
+    """The CPU oracle is test infrastructure; built here only so build() can
+    prepare it next to the product."""
+    res = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], capture_output=True,
+                         text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"oracle build failed:\n{res.stdout}\n{res.stderr}")
+    return os.path.join(ROOT, "oracle", "liboracle.so")
+
+
+if __name__ == "__main__":
+    print(build_library(force="--force" in sys.argv, verbose=True))
+    if "--all" in sys.argv:
+        print(build_oracle())

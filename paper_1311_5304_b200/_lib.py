@@ -1,0 +1,160 @@
+"""ctypes binding of libhetjpeg_b200.so (C ABI: include/hetjpeg_b200.h).
+
+The product path has no CPU fallback: importing this module fails loudly
+(ImportError) when the library is missing, and every compute call raises when
+no CUDA device is visible.  Build with `python -m paper_1311_5304_b200._build`
+(or `__graft_entry__.build()`).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .errors import BadCode, BitstreamExhausted, HetJpegError, MarkerInScan
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhetjpeg_b200.so")
+
+HJ_OK = 0
+HJ_ERR_EXHAUSTED = 1
+HJ_ERR_BADCODE = 2
+HJ_ERR_MARKER = 3
+HJ_ERR_RST_SEQ = 4
+HJ_ERR_ARG = 16
+HJ_ERR_CUDA = 17
+HJ_ERR_NOMEM = 18
+HJ_ERR_NODEVICE = 19
+
+SUB_444, SUB_422, SUB_420 = 0, 1, 2
+FLAG_DIRECT_IDCT = 1
+
+
+class CudaError(HetJpegError, RuntimeError):
+    """A CUDA runtime failure inside the native library."""
+
+
+class NoDevice(HetJpegError, RuntimeError):
+    """No CUDA device is visible: the parallel phase has no CPU fallback."""
+
+
+class hj_image_t(C.Structure):  # noqa: N801 - C name
+    _fields_ = [
+        ("y", C.c_void_p), ("cb", C.c_void_p), ("cr", C.c_void_p), ("q", C.c_void_p),
+        ("rgb", C.c_void_p),
+        ("width", C.c_int32), ("height", C.c_int32),
+        ("mcus_per_row", C.c_int32), ("mcu_rows", C.c_int32),
+        ("row0", C.c_int32), ("n_rows", C.c_int32),
+        ("subsampling", C.c_int32), ("flags", C.c_int32),
+    ]
+
+
+class hj_scan_tables_t(C.Structure):  # noqa: N801
+    _fields_ = [
+        ("lut_sym", C.c_uint8 * 256 * 8), ("lut_len", C.c_uint8 * 256 * 8),
+        ("mincode", C.c_int32 * 17 * 8), ("maxcode", C.c_int32 * 17 * 8),
+        ("valptr", C.c_int32 * 17 * 8), ("symbols", C.c_uint8 * 256 * 8),
+        ("comp_dc", C.c_int32 * 3), ("comp_ac", C.c_int32 * 3),
+    ]
+
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(
+        f"native library missing: {_LIB_PATH} (build it with "
+        "`python -m paper_1311_5304_b200._build`); there is no CPU fallback")
+
+lib = C.CDLL(_LIB_PATH)
+
+_P = C.c_void_p
+_I32 = C.c_int32
+_I64 = C.c_int64
+_SIG = {
+    "hj_version": (C.c_char_p, []),
+    "hj_last_error": (C.c_char_p, []),
+    "hj_device_count": (C.c_int, []),
+    "hj_set_device": (C.c_int, [C.c_int]),
+    "hj_malloc_device": (C.c_int, [C.POINTER(_P), C.c_size_t]),
+    "hj_free_device": (C.c_int, [_P]),
+    "hj_malloc_host": (C.c_int, [C.POINTER(_P), C.c_size_t]),
+    "hj_free_host": (C.c_int, [_P]),
+    "hj_memcpy_h2d": (C.c_int, [_P, _P, C.c_size_t, _P]),
+    "hj_memcpy_d2h": (C.c_int, [_P, _P, C.c_size_t, _P]),
+    "hj_memset_device": (C.c_int, [_P, C.c_int, C.c_size_t, _P]),
+    "hj_stream_create": (C.c_int, [C.POINTER(_P)]),
+    "hj_stream_destroy": (C.c_int, [_P]),
+    "hj_stream_synchronize": (C.c_int, [_P]),
+    "hj_device_synchronize": (C.c_int, []),
+    "hj_event_create": (C.c_int, [C.POINTER(_P)]),
+    "hj_event_destroy": (C.c_int, [_P]),
+    "hj_event_record": (C.c_int, [_P, _P]),
+    "hj_event_elapsed_ms": (C.c_int, [_P, _P, C.POINTER(C.c_float)]),
+    "hj_render_batch": (C.c_int, [C.POINTER(hj_image_t), C.c_int, _P]),
+    "hj_plan_create": (C.c_int, [C.POINTER(hj_image_t), C.c_int, C.POINTER(_P)]),
+    "hj_plan_launch": (C.c_int, [_P, _P]),
+    "hj_plan_destroy": (C.c_int, [_P]),
+    "hj_launch_count": (C.c_uint64, []),
+    "hj_render_rows": (C.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
+                                 _I32, _I32, _I64, _I64]),
+    "hj_idct_blocks": (C.c_int, [_P, _I64, _P, _I32]),
+    "hj_idct_blocks_f64": (C.c_int, [_P, _I64, _P, _I32]),
+    "hj_ycbcr_to_rgb": (C.c_int, [_P, _P, _P, _P, _I64]),
+    "hj_upsample_422": (C.c_int, [_P, _P, _P, _P, _I64]),
+    "hj_decode_mcu_rows": (C.c_int, [_P, _I64, _P, C.POINTER(hj_scan_tables_t), _P, _P, _P, _I32,
+                                     _I32, _I32, _I32, _I32]),
+    "hj_scan_entropy_end": (C.c_int64, [_P, _I64, _I64]),
+}
+for _name, (_res, _args) in _SIG.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+EXPORTED = tuple(_SIG)
+
+
+def last_error() -> str:
+    return lib.hj_last_error().decode(errors="replace")
+
+
+def check(status: int, what: str = "") -> None:
+    """Map an hj_status onto the reference exception classes."""
+    if status == HJ_OK:
+        return
+    msg = last_error() or what
+    if status == HJ_ERR_EXHAUSTED:
+        raise BitstreamExhausted("ran out of entropy-coded bits")
+    if status == HJ_ERR_BADCODE:
+        raise BadCode("no Huffman symbol matches within 16 bits")
+    if status == HJ_ERR_MARKER:
+        raise MarkerInScan("non-restart marker inside the scan")
+    if status == HJ_ERR_RST_SEQ:
+        raise MarkerInScan("restart marker out of sequence")
+    if status == HJ_ERR_ARG:
+        raise ValueError(msg)
+    if status == HJ_ERR_NODEVICE:
+        raise NoDevice(msg)
+    raise CudaError(f"{what}: {msg}")
+
+
+_device_lock = threading.Lock()
+_device_ready = False
+
+
+def require_device() -> None:
+    """Fail loudly when no GPU is visible (no CPU fallback exists)."""
+    global _device_ready
+    if _device_ready:
+        return
+    with _device_lock:
+        if lib.hj_device_count() <= 0:
+            raise NoDevice("no CUDA device visible; the hetjpeg-b200 parallel phase "
+                           "runs only on the GPU")
+        _device_ready = True
+
+
+def ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def version() -> str:
+    return lib.hj_version().decode()

@@ -1,0 +1,485 @@
+// C-ABI host layer of libhetjpeg_b200.so (declared in include/hetjpeg_b200.h).
+//
+// Owns: per-thread error strings, per-thread synchronous contexts (stream +
+// device staging for the drop-in render_rows), tile planning for batched
+// launches, and thin wrappers over device memory so a host language needs
+// nothing but this library (ctypes, cgo, JNI ...).
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "hj_render.cuh"
+
+namespace {
+
+thread_local std::string t_error;
+std::atomic<uint64_t> g_launches{0};
+
+hj_status fail(hj_status code, const std::string &msg) {
+    t_error = msg;
+    return code;
+}
+
+hj_status cuda_fail(cudaError_t e, const char *what) {
+    return fail(HJ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define HJ_CUDA(call)                                           \
+    do {                                                        \
+        cudaError_t e_ = (call);                                \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);     \
+    } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int ypm_of(int sub) { return sub == HJ_SUB_444 ? 1 : sub == HJ_SUB_422 ? 2 : 4; }
+int mcu_w_of(int sub) { return sub == HJ_SUB_444 ? 8 : 16; }
+int mcu_h_of(int sub) { return sub == HJ_SUB_420 ? 16 : 8; }
+
+hj_status validate(const hj_image_t &im) {
+    if (im.subsampling < HJ_SUB_444 || im.subsampling > HJ_SUB_420)
+        return fail(HJ_ERR_ARG, "unknown subsampling " + std::to_string(im.subsampling));
+    if (im.width < 1 || im.height < 1) return fail(HJ_ERR_ARG, "zero image dimension");
+    int mw = mcu_w_of(im.subsampling), mh = mcu_h_of(im.subsampling);
+    if (im.mcus_per_row != (im.width + mw - 1) / mw || im.mcu_rows != (im.height + mh - 1) / mh)
+        return fail(HJ_ERR_ARG, "mcus_per_row/mcu_rows do not match the image geometry");
+    if (im.row0 < 0 || im.n_rows < 0 || im.row0 + im.n_rows > im.mcu_rows)
+        return fail(HJ_ERR_ARG, "MCU row range outside the image");
+    if (!im.y || !im.cb || !im.cr || !im.q || !im.rgb) return fail(HJ_ERR_ARG, "null pointer");
+    return HJ_OK;
+}
+
+// Tile planning: strips of ~kStrip MCU columns, row segments of T rows, with
+// T chosen so the whole batch gives ~6 waves of CTAs (3 resident per SM).
+struct Plan {
+    // device buffer: [hj_image_t x n_images][Tile x n_tiles]
+    void *dev = nullptr;
+    size_t bytes = 0;
+    size_t tile_base = 0;  // byte offset of the Tile array in dev
+    int n_images = 0;
+    struct Group { int sub; bool direct; int offset; int count; };
+    std::vector<Group> groups;
+};
+
+void build_tiles(const hj_image_t *images, int n, std::vector<hj::Tile> &tiles,
+                 std::vector<Plan::Group> &groups) {
+    int sms = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t target = (int64_t)sms * 3 * 6;
+    for (int sub = HJ_SUB_444; sub <= HJ_SUB_420; ++sub) {
+        for (int direct = 0; direct < 2; ++direct) {
+            int64_t strip_rows = 0;
+            for (int i = 0; i < n; ++i) {
+                const hj_image_t &im = images[i];
+                if (im.subsampling != sub || ((im.flags & HJ_FLAG_DIRECT_IDCT) != 0) != (direct != 0)) continue;
+                int S = hj::strip_width(sub);
+                int ns = (im.mcus_per_row + S - 1) / S;
+                strip_rows += (int64_t)ns * im.n_rows;
+            }
+            if (strip_rows == 0) continue;
+            int T = (int)std::min<int64_t>(64, std::max<int64_t>(1, (strip_rows + target - 1) / target));
+            Plan::Group g{sub, direct != 0, (int)tiles.size(), 0};
+            for (int i = 0; i < n; ++i) {
+                const hj_image_t &im = images[i];
+                if (im.subsampling != sub || ((im.flags & HJ_FLAG_DIRECT_IDCT) != 0) != (direct != 0)) continue;
+                int S = hj::strip_width(sub);
+                int ns = (im.mcus_per_row + S - 1) / S;
+                for (int r = im.row0; r < im.row0 + im.n_rows; r += T) {
+                    int r1 = std::min(im.row0 + im.n_rows, r + T);
+                    for (int s = 0; s < ns; ++s) {
+                        hj::Tile t{};
+                        t.image = i;
+                        t.m0 = (int)((int64_t)s * im.mcus_per_row / ns);
+                        t.m1 = (int)((int64_t)(s + 1) * im.mcus_per_row / ns);
+                        t.r0 = r;
+                        t.r1 = r1;
+                        tiles.push_back(t);
+                    }
+                }
+            }
+            g.count = (int)tiles.size() - g.offset;
+            groups.push_back(g);
+        }
+    }
+}
+
+hj_status plan_create(const hj_image_t *images, int n, Plan **out, cudaStream_t stream) {
+    if (n < 0 || (n > 0 && !images)) return fail(HJ_ERR_ARG, "bad image array");
+    for (int i = 0; i < n; ++i) {
+        hj_status s = validate(images[i]);
+        if (s != HJ_OK) return s;
+    }
+    std::vector<hj::Tile> tiles;
+    Plan *p = new Plan();
+    build_tiles(images, n, tiles, p->groups);
+    p->n_images = n;
+    size_t img_bytes = ((sizeof(hj_image_t) * (size_t)n + 255) / 256) * 256;
+    p->bytes = img_bytes + sizeof(hj::Tile) * tiles.size();
+    if (p->bytes > 0) {
+        cudaError_t e = cudaMalloc(&p->dev, p->bytes);
+        if (e != cudaSuccess) {
+            delete p;
+            return cuda_fail(e, "cudaMalloc(plan)");
+        }
+        std::vector<uint8_t> host(p->bytes);
+        if (n) std::memcpy(host.data(), images, sizeof(hj_image_t) * n);
+        if (!tiles.empty()) std::memcpy(host.data() + img_bytes, tiles.data(), sizeof(hj::Tile) * tiles.size());
+        e = cudaMemcpyAsync(p->dev, host.data(), p->bytes, cudaMemcpyHostToDevice, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) {
+            cudaFree(p->dev);
+            delete p;
+            return cuda_fail(e, "upload plan");
+        }
+        p->tile_base = img_bytes;
+    }
+    *out = p;
+    return HJ_OK;
+}
+
+hj_status plan_launch(const Plan *p, cudaStream_t stream) {
+    if (!p || !p->dev) return HJ_OK;
+    const hj_image_t *imgs = reinterpret_cast<const hj_image_t *>(p->dev);
+    const hj::Tile *tiles = reinterpret_cast<const hj::Tile *>(static_cast<uint8_t *>(p->dev) + p->tile_base);
+    for (const auto &g : p->groups) {
+        cudaError_t e = hj::launch_render(g.sub, g.direct, imgs, tiles + g.offset, g.count, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "render kernel launch");
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    return HJ_OK;
+}
+
+// Per-thread context of the synchronous drop-in API.
+struct SyncCtx {
+    cudaStream_t stream = nullptr;
+    int device = -1;
+    void *coef = nullptr;
+    size_t coef_bytes = 0;
+    void *rgb = nullptr;
+    size_t rgb_bytes = 0;
+    void *misc = nullptr;  // q (768 B) + image desc + tiles
+    size_t misc_bytes = 0;
+    ~SyncCtx() {
+        if (device >= 0) {
+            cudaFree(coef);
+            cudaFree(rgb);
+            cudaFree(misc);
+            if (stream) cudaStreamDestroy(stream);
+        }
+    }
+};
+thread_local SyncCtx t_ctx;
+
+hj_status ensure(void **p, size_t *have, size_t need) {
+    if (*have >= need) return HJ_OK;
+    size_t n = std::max(need, *have * 2);
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+    HJ_CUDA(cudaMalloc(p, n));
+    *have = n;
+    return HJ_OK;
+}
+
+hj_status ctx_get(SyncCtx **out) {
+    int dev = 0;
+    HJ_CUDA(cudaGetDevice(&dev));
+    SyncCtx &c = t_ctx;
+    if (c.device != dev) {
+        if (c.device >= 0) {
+            cudaFree(c.coef);
+            cudaFree(c.rgb);
+            cudaFree(c.misc);
+            if (c.stream) cudaStreamDestroy(c.stream);
+            c = SyncCtx();
+        }
+        HJ_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        c.device = dev;
+    }
+    *out = &c;
+    return HJ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *hj_version(void) { return "hetjpeg-b200 0.1.0 (sm_100a)"; }
+const char *hj_last_error(void) { return t_error.c_str(); }
+
+int hj_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+hj_status hj_set_device(int device) {
+    int n = hj_device_count();
+    if (n == 0) return fail(HJ_ERR_NODEVICE, "no CUDA device visible");
+    if (device < 0 || device >= n) return fail(HJ_ERR_ARG, "device index out of range");
+    HJ_CUDA(cudaSetDevice(device));
+    return HJ_OK;
+}
+
+hj_status hj_malloc_device(void **ptr, size_t bytes) {
+    if (!ptr) return fail(HJ_ERR_ARG, "null out pointer");
+    HJ_CUDA(cudaMalloc(ptr, bytes ? bytes : 1));
+    return HJ_OK;
+}
+hj_status hj_free_device(void *ptr) {
+    HJ_CUDA(cudaFree(ptr));
+    return HJ_OK;
+}
+hj_status hj_malloc_host(void **ptr, size_t bytes) {
+    if (!ptr) return fail(HJ_ERR_ARG, "null out pointer");
+    HJ_CUDA(cudaMallocHost(ptr, bytes ? bytes : 1));
+    return HJ_OK;
+}
+hj_status hj_free_host(void *ptr) {
+    HJ_CUDA(cudaFreeHost(ptr));
+    return HJ_OK;
+}
+hj_status hj_memcpy_h2d(void *dst, const void *src, size_t bytes, void *stream) {
+    HJ_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, as_stream(stream)));
+    return HJ_OK;
+}
+hj_status hj_memcpy_d2h(void *dst, const void *src, size_t bytes, void *stream) {
+    HJ_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream)));
+    return HJ_OK;
+}
+hj_status hj_memset_device(void *dst, int value, size_t bytes, void *stream) {
+    HJ_CUDA(cudaMemsetAsync(dst, value, bytes, as_stream(stream)));
+    return HJ_OK;
+}
+hj_status hj_stream_create(void **stream) {
+    cudaStream_t s;
+    HJ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    *stream = s;
+    return HJ_OK;
+}
+hj_status hj_stream_destroy(void *stream) {
+    HJ_CUDA(cudaStreamDestroy(as_stream(stream)));
+    return HJ_OK;
+}
+hj_status hj_stream_synchronize(void *stream) {
+    HJ_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    return HJ_OK;
+}
+hj_status hj_device_synchronize(void) {
+    HJ_CUDA(cudaDeviceSynchronize());
+    return HJ_OK;
+}
+hj_status hj_event_create(void **event) {
+    cudaEvent_t e;
+    HJ_CUDA(cudaEventCreate(&e));
+    *event = e;
+    return HJ_OK;
+}
+hj_status hj_event_destroy(void *event) {
+    HJ_CUDA(cudaEventDestroy(reinterpret_cast<cudaEvent_t>(event)));
+    return HJ_OK;
+}
+hj_status hj_event_record(void *event, void *stream) {
+    HJ_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(event), as_stream(stream)));
+    return HJ_OK;
+}
+hj_status hj_event_elapsed_ms(void *start, void *end, float *ms) {
+    HJ_CUDA(cudaEventElapsedTime(ms, reinterpret_cast<cudaEvent_t>(start), reinterpret_cast<cudaEvent_t>(end)));
+    return HJ_OK;
+}
+
+hj_status hj_plan_create(const hj_image_t *images, int n_images, void **plan) {
+    if (!plan) return fail(HJ_ERR_ARG, "null plan pointer");
+    Plan *p = nullptr;
+    hj_status s = plan_create(images, n_images, &p, nullptr);
+    if (s != HJ_OK) return s;
+    *plan = p;
+    return HJ_OK;
+}
+
+hj_status hj_plan_launch(void *plan, void *stream) {
+    return plan_launch(static_cast<Plan *>(plan), as_stream(stream));
+}
+
+hj_status hj_plan_destroy(void *plan) {
+    Plan *p = static_cast<Plan *>(plan);
+    if (!p) return HJ_OK;
+    if (p->dev) cudaFree(p->dev);
+    delete p;
+    return HJ_OK;
+}
+
+hj_status hj_render_batch(const hj_image_t *images, int n_images, void *stream) {
+    Plan *p = nullptr;
+    hj_status s = plan_create(images, n_images, &p, as_stream(stream));
+    if (s != HJ_OK) return s;
+    s = plan_launch(p, as_stream(stream));
+    cudaError_t e = cudaStreamSynchronize(as_stream(stream));
+    hj_plan_destroy(p);
+    if (s != HJ_OK) return s;
+    if (e != cudaSuccess) return cuda_fail(e, "render batch");
+    return HJ_OK;
+}
+
+uint64_t hj_launch_count(void) { return g_launches.load(); }
+
+hj_status hj_render_rows(const int16_t *y, const int16_t *cb, const int16_t *cr,
+                         const int32_t *q3x64, uint8_t *rgb, int32_t width, int32_t height,
+                         int32_t mcus_per_row, int32_t mcu_rows, int32_t row0, int32_t n_rows,
+                         int32_t subsampling, int32_t fast, int32_t fused,
+                         int64_t n_y_blocks, int64_t n_c_blocks) {
+    (void)fused;  // fused and unfused paths are byte-identical (fallback.py:230-234)
+    if (n_rows <= 0) return HJ_OK;  // block_transforms.py:66-67
+    if (!y || !cb || !cr || !q3x64 || !rgb) return fail(HJ_ERR_ARG, "null pointer");
+    hj_image_t im{};
+    im.width = width;
+    im.height = height;
+    im.mcus_per_row = mcus_per_row;
+    im.mcu_rows = mcu_rows;
+    im.row0 = row0;
+    im.n_rows = n_rows;
+    im.subsampling = subsampling;
+    im.flags = fast ? 0 : HJ_FLAG_DIRECT_IDCT;
+    im.y = im.cb = im.cr = reinterpret_cast<const int16_t *>(16);  // placeholders for validate
+    im.q = reinterpret_cast<const int32_t *>(16);
+    im.rgb = reinterpret_cast<uint8_t *>(16);
+    hj_status st = validate(im);
+    if (st != HJ_OK) return st;
+    const int ypm = ypm_of(subsampling), mh = mcu_h_of(subsampling);
+    // coefficient MCU rows the kernel reads (4:2:0: +-1 row of chroma context)
+    int c_lo = row0, c_hi = row0 + n_rows;
+    if (subsampling == HJ_SUB_420) {
+        c_lo = std::max(0, row0 - 1);
+        c_hi = std::min(mcu_rows, row0 + n_rows + 1);
+    }
+    const int64_t per_row_c = mcus_per_row;
+    const int64_t per_row_y = (int64_t)mcus_per_row * ypm;
+    if ((int64_t)c_hi * per_row_c > n_c_blocks || (int64_t)(row0 + n_rows) * per_row_y > n_y_blocks)
+        return fail(HJ_ERR_ARG, "coefficient planes smaller than the MCU rows requested");
+    const int64_t nyb = (int64_t)n_rows * per_row_y;
+    const int64_t ncb = (int64_t)(c_hi - c_lo) * per_row_c;
+    const int py0 = row0 * mh, py1 = std::min(height, (row0 + n_rows) * mh);
+    const size_t rgb_bytes = (size_t)(py1 - py0) * width * 3;
+
+    SyncCtx *c = nullptr;
+    st = ctx_get(&c);
+    if (st != HJ_OK) return st;
+    const size_t coef_bytes = (size_t)(nyb + 2 * ncb) * 128;
+    st = ensure(&c->coef, &c->coef_bytes, coef_bytes);
+    if (st == HJ_OK) st = ensure(&c->rgb, &c->rgb_bytes, std::max<size_t>(rgb_bytes, 16));
+    // misc: q (768 B, 256-aligned slot) + plan image/tiles are built separately
+    if (st == HJ_OK) st = ensure(&c->misc, &c->misc_bytes, 1024);
+    if (st != HJ_OK) return st;
+    int16_t *dy = static_cast<int16_t *>(c->coef);
+    int16_t *dcb = dy + nyb * 64;
+    int16_t *dcr = dcb + ncb * 64;
+    int32_t *dq = static_cast<int32_t *>(c->misc);
+    HJ_CUDA(cudaMemcpyAsync(dy, y + (int64_t)row0 * per_row_y * 64, nyb * 128, cudaMemcpyHostToDevice, c->stream));
+    HJ_CUDA(cudaMemcpyAsync(dcb, cb + (int64_t)c_lo * per_row_c * 64, ncb * 128, cudaMemcpyHostToDevice, c->stream));
+    HJ_CUDA(cudaMemcpyAsync(dcr, cr + (int64_t)c_lo * per_row_c * 64, ncb * 128, cudaMemcpyHostToDevice, c->stream));
+    HJ_CUDA(cudaMemcpyAsync(dq, q3x64, 768, cudaMemcpyHostToDevice, c->stream));
+    // virtual bases so the kernel indexes whole-image block / pixel coordinates
+    im.y = dy - (int64_t)row0 * per_row_y * 64;
+    im.cb = dcb - (int64_t)c_lo * per_row_c * 64;
+    im.cr = dcr - (int64_t)c_lo * per_row_c * 64;
+    im.q = dq;
+    im.rgb = static_cast<uint8_t *>(c->rgb) - (int64_t)py0 * width * 3;
+    Plan *p = nullptr;
+    st = plan_create(&im, 1, &p, c->stream);
+    if (st != HJ_OK) return st;
+    st = plan_launch(p, c->stream);
+    if (st == HJ_OK) {
+        cudaError_t e = cudaMemcpyAsync(rgb + (size_t)py0 * width * 3, c->rgb, rgb_bytes,
+                                        cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) st = cuda_fail(e, "render_rows");
+    }
+    hj_plan_destroy(p);
+    return st;
+}
+
+static hj_status run_blocks(const int32_t *deq, int64_t n, uint8_t *out, double *out_f64, int32_t fast) {
+    if (n < 0) return fail(HJ_ERR_ARG, "negative block count");
+    if (n == 0) return HJ_OK;
+    SyncCtx *c = nullptr;
+    hj_status st = ctx_get(&c);
+    if (st != HJ_OK) return st;
+    size_t in_b = (size_t)n * 256, out_b = (size_t)n * 64 * (out_f64 ? 8 : 1);
+    st = ensure(&c->coef, &c->coef_bytes, in_b);
+    if (st == HJ_OK) st = ensure(&c->rgb, &c->rgb_bytes, out_b);
+    if (st != HJ_OK) return st;
+    HJ_CUDA(cudaMemcpyAsync(c->coef, deq, in_b, cudaMemcpyHostToDevice, c->stream));
+    cudaError_t e = hj::launch_idct_blocks(static_cast<int32_t *>(c->coef), n,
+                                           out_f64 ? nullptr : static_cast<uint8_t *>(c->rgb),
+                                           out_f64 ? static_cast<double *>(c->rgb) : nullptr, !fast, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "idct_blocks launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    HJ_CUDA(cudaMemcpyAsync(out_f64 ? static_cast<void *>(out_f64) : static_cast<void *>(out), c->rgb, out_b,
+                            cudaMemcpyDeviceToHost, c->stream));
+    HJ_CUDA(cudaStreamSynchronize(c->stream));
+    return HJ_OK;
+}
+
+hj_status hj_idct_blocks(const int32_t *deq, int64_t n, uint8_t *out, int32_t fast) {
+    if (!deq || !out) return fail(HJ_ERR_ARG, "null pointer");
+    return run_blocks(deq, n, out, nullptr, fast);
+}
+
+hj_status hj_idct_blocks_f64(const int32_t *deq, int64_t n, double *out, int32_t fast) {
+    if (!deq || !out) return fail(HJ_ERR_ARG, "null pointer");
+    return run_blocks(deq, n, nullptr, out, fast);
+}
+
+hj_status hj_ycbcr_to_rgb(const uint8_t *y, const uint8_t *cb, const uint8_t *cr, uint8_t *rgb, int64_t n) {
+    if (n < 0 || !y || !cb || !cr || !rgb) return fail(HJ_ERR_ARG, "bad arguments");
+    if (n == 0) return HJ_OK;
+    SyncCtx *c = nullptr;
+    hj_status st = ctx_get(&c);
+    if (st != HJ_OK) return st;
+    st = ensure(&c->coef, &c->coef_bytes, (size_t)n * 3);
+    if (st == HJ_OK) st = ensure(&c->rgb, &c->rgb_bytes, (size_t)n * 3);
+    if (st != HJ_OK) return st;
+    uint8_t *d = static_cast<uint8_t *>(c->coef);
+    HJ_CUDA(cudaMemcpyAsync(d, y, n, cudaMemcpyHostToDevice, c->stream));
+    HJ_CUDA(cudaMemcpyAsync(d + n, cb, n, cudaMemcpyHostToDevice, c->stream));
+    HJ_CUDA(cudaMemcpyAsync(d + 2 * n, cr, n, cudaMemcpyHostToDevice, c->stream));
+    cudaError_t e = hj::launch_ycbcr(d, d + n, d + 2 * n, static_cast<uint8_t *>(c->rgb), n, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "ycbcr launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    HJ_CUDA(cudaMemcpyAsync(rgb, c->rgb, (size_t)n * 3, cudaMemcpyDeviceToHost, c->stream));
+    HJ_CUDA(cudaStreamSynchronize(c->stream));
+    return HJ_OK;
+}
+
+hj_status hj_upsample_422(const uint8_t *rows, const int16_t *left, const int16_t *right,
+                          int32_t *out, int64_t n) {
+    if (n < 0 || !rows || !left || !right || !out) return fail(HJ_ERR_ARG, "bad arguments");
+    if (n == 0) return HJ_OK;
+    SyncCtx *c = nullptr;
+    hj_status st = ctx_get(&c);
+    if (st != HJ_OK) return st;
+    st = ensure(&c->coef, &c->coef_bytes, (size_t)n * 12);
+    if (st == HJ_OK) st = ensure(&c->rgb, &c->rgb_bytes, (size_t)n * 64);
+    if (st != HJ_OK) return st;
+    uint8_t *d = static_cast<uint8_t *>(c->coef);
+    int16_t *dl = reinterpret_cast<int16_t *>(d + n * 8);
+    int16_t *dr = dl + n;
+    HJ_CUDA(cudaMemcpyAsync(d, rows, n * 8, cudaMemcpyHostToDevice, c->stream));
+    HJ_CUDA(cudaMemcpyAsync(dl, left, n * 2, cudaMemcpyHostToDevice, c->stream));
+    HJ_CUDA(cudaMemcpyAsync(dr, right, n * 2, cudaMemcpyHostToDevice, c->stream));
+    cudaError_t e = hj::launch_upsample_422(d, dl, dr, static_cast<int32_t *>(c->rgb), n, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "upsample launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    HJ_CUDA(cudaMemcpyAsync(out, c->rgb, (size_t)n * 64, cudaMemcpyDeviceToHost, c->stream));
+    HJ_CUDA(cudaStreamSynchronize(c->stream));
+    return HJ_OK;
+}
+
+}  // extern "C"

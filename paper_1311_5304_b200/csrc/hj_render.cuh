@@ -1,0 +1,47 @@
+// Internal interface between the C-ABI host layer (hj_api.cu) and the
+// sm_100a render kernels (hj_render.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/hetjpeg_b200.h"
+
+namespace hj {
+
+// A CTA's work unit: one vertical strip of MCU columns [m0, m1) of one
+// image, swept over MCU rows [r0, r1).  The sweep carries the chroma rows
+// of the previous MCU row (4:2:0 vertical context) in shared memory.
+struct Tile {
+    int32_t image;
+    int32_t m0, m1;
+    int32_t r0, r1;
+    int32_t pad[3];
+};
+static_assert(sizeof(Tile) == 32, "Tile layout");
+
+// Strip widths (MCUs per CTA) chosen so one sweep step has ~128 blocks for
+// the 128 threads of the CTA: 444 -> 3*S, 422 -> 4*S+4, 420 -> 6*S+4.
+constexpr int kThreads = 128;
+constexpr int kStrip444 = 42;
+constexpr int kStrip422 = 31;
+constexpr int kStrip420 = 20;
+
+inline int strip_width(int sub) {
+    return sub == HJ_SUB_444 ? kStrip444 : sub == HJ_SUB_422 ? kStrip422 : kStrip420;
+}
+
+// Launch the render kernel for `n_tiles` tiles of one subsampling family.
+// `images` and `tiles` are device arrays.
+cudaError_t launch_render(int subsampling, bool direct, const hj_image_t *images,
+                          const Tile *tiles, int n_tiles, cudaStream_t stream);
+
+// Single-block transforms (reference per-block API).
+cudaError_t launch_idct_blocks(const int32_t *deq, int64_t n, uint8_t *out, double *out_f64,
+                               bool direct, cudaStream_t stream);
+cudaError_t launch_upsample_422(const uint8_t *rows, const int16_t *left, const int16_t *right,
+                               int32_t *out, int64_t n, cudaStream_t stream);
+cudaError_t launch_ycbcr(const uint8_t *y, const uint8_t *cb, const uint8_t *cr, uint8_t *rgb,
+                         int64_t n, cudaStream_t stream);
+
+}  // namespace hj

@@ -1,0 +1,207 @@
+"""Parity of the sm_100a parallel phase with the reference (golden fixtures:
+the reference's own render_rows output for 4:4:4/4:2:2) and with the CPU
+oracle (4:2:0 extension, full BASELINE sizes, adversarial inputs).
+Bar: bit-exact RGB.  Calls go through the C ABI (ctypes)."""
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_CASES
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+RENDER = {0: "render_rows_444", 1: "render_rows_422", 2: "render_rows_420"}
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    from paper_1311_5304_b200 import _lib
+    from paper_1311_5304_b200.kernels import cuda as backend
+    _lib.require_device()
+    return backend
+
+
+def _render(cuda, g, fast=True, row0=0, n_rows=None, rgb=None, y=None, cb=None, cr=None, q=None):
+    mh = 16 if g.sub == 2 else 8
+    mw = 8 if g.sub == 0 else 16
+    rows = -(-g.height // mh)
+    n_rows = rows - row0 if n_rows is None else n_rows
+    rgb = np.zeros((g.height, g.width, 3), np.uint8) if rgb is None else rgb
+    getattr(cuda, RENDER[g.sub])(g.y if y is None else y, g.cb if cb is None else cb,
+                                 g.cr if cr is None else cr, g.q if q is None else q, rgb,
+                                 g.width, g.height, -(-g.width // mw), row0, n_rows, fast, True)
+    return rgb
+
+
+@pytest.mark.parametrize("g", GOLDEN_CASES, ids=repr)
+@pytest.mark.parametrize("fast", [True, False], ids=["aan", "direct"])
+def test_render_matches_golden(cuda, g, fast):
+    assert np.array_equal(_render(cuda, g, fast), g.rgb if fast else g.rgb_direct)
+
+
+@pytest.mark.parametrize("g", [c for c in GOLDEN_CASES if c.meta["mcu_rows"] >= 3], ids=repr)
+def test_partial_row_ranges(cuda, g):
+    rows = g.meta["mcu_rows"]
+    rng = np.random.default_rng(len(g.name))
+    rgb = np.full((g.height, g.width, 3), 7, np.uint8)
+    r = 0
+    while r < rows:
+        n = int(rng.integers(1, 4))
+        n = min(n, rows - r)
+        _render(cuda, g, True, r, n, rgb)
+        r += n
+    assert np.array_equal(rgb, g.rgb)
+    # a zero-row call is a no-op
+    _render(cuda, g, True, 0, 0, rgb)
+
+
+def test_concurrent_disjoint_ranges(cuda):
+    g = max((c for c in GOLDEN_CASES if c.sub == 1), key=lambda c: c.width * c.height)
+    rows = g.meta["mcu_rows"]
+    rgb = np.zeros((g.height, g.width, 3), np.uint8)
+    spans = [(r, min(4, rows - r)) for r in range(0, rows, 4)]
+    errs = []
+
+    def work(chunk):
+        try:
+            for r0, n in chunk:
+                _render(cuda, g, True, r0, n, rgb)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(spans[i::4],)) for i in range(4)]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    assert not errs
+    assert np.array_equal(rgb, g.rgb)
+
+
+def test_idct_blocks_match_reference(blocks_golden):
+    from paper_1311_5304_b200 import block_transforms as bt
+    deq = blocks_golden["deq"]
+    assert np.array_equal(bt.idct_fast(deq), blocks_golden["fast"])
+    assert np.array_equal(bt.idct_direct(deq), blocks_golden["direct"])
+    f64 = bt.idct_fast_f64(deq[:256]).reshape(256, 64)
+    assert np.array_equal(f64.view(np.uint64), blocks_golden["f64_fast"].view(np.uint64))
+    f64d = bt.idct_direct_f64(deq[:256]).reshape(256, 64)
+    assert np.array_equal(f64d.view(np.uint64), blocks_golden["f64_direct"].view(np.uint64))
+    # SPEC.md:173-174,181-182
+    z = np.zeros(64, np.int32)
+    dc = z.copy()
+    dc[0] = 240
+    assert (bt.idct_fast(z) == 128).all() and (bt.idct_direct(dc) == 158).all()
+
+
+def test_colour_exhaustive_on_gpu():
+    from paper_1311_5304_b200 import block_transforms as bt
+    v = np.arange(256, dtype=np.uint8)
+    y, cb, cr = (a.reshape(-1) for a in np.meshgrid(v, v, v, indexing="ij"))
+    r, g, b = bt.ycbcr_to_rgb(y, cb, cr)
+    want = oracle.ycbcr_to_rgb(y, cb, cr)
+    assert np.array_equal(np.stack([r, g, b], -1), want)
+    # SPEC.md:199-201
+    assert [int(c) for c in bt.ycbcr_to_rgb(76, 85, 255)] == [254, 0, 0]
+
+
+def test_upsample_row_422_spec():
+    from paper_1311_5304_b200 import block_transforms as bt
+    ramp = np.arange(0, 32, 4)
+    assert bt.upsample_row_422(ramp).tolist() == [0, 1, 3, 5, 7, 9, 11, 13, 15, 17, 19, 21, 23,
+                                                  25, 27, 28]
+    assert (bt.upsample_row_422([9] * 8) == 9).all()
+    out = bt.upsample_row_422(ramp, left=10, right=40)
+    assert out[0] == (0 * 3 + 10 + 1) // 4 and out[15] == (28 * 3 + 40 + 2) // 4
+    rgb = bt.fused_upsample_color_422(np.full(16, 90), ramp, ramp[::-1])
+    r, g, b = bt.ycbcr_to_rgb(np.full(16, 90), bt.upsample_row_422(ramp),
+                              bt.upsample_row_422(ramp[::-1]))
+    assert np.array_equal(rgb, np.stack([r, g, b], -1))
+
+
+def test_fused_444_single_mcu(cuda):
+    from paper_1311_5304_b200 import block_transforms as bt
+    rng = np.random.default_rng(3)
+    blocks = rng.integers(-60, 60, size=(3, 64)).astype(np.int16)
+    q = rng.integers(1, 40, size=(3, 64)).astype(np.int32)
+    got = bt.fused_idct_color_444(blocks[0], blocks[1], blocks[2], q[0], q[1], q[2])
+    want = oracle.render(blocks[0:1], blocks[1:2], blocks[2:3], q, 8, 8, 0)
+    assert np.array_equal(got, want.reshape(64, 3))
+
+
+def _synthetic(width, height, quality, sub, **kw):
+    from paper_1311_5304_b200 import entropy, parser
+    from paper_1311_5304_b200.perf_model import qtable_stack
+    from paper_1311_5304_b200.synth import synth_jpeg
+    blob = synth_jpeg(width, height, quality, sub, **kw)
+    p = parser.parse_stream(blob)
+    coeffs, _ = entropy.decode_all(p, blob)
+    return p, coeffs, qtable_stack(p)
+
+
+@pytest.mark.parametrize("w,h,q,sub,kw", [
+    (512, 512, 75, "420", {}),
+    (1920, 1080, 90, "420", {}),
+    (4096, 4096, 95, "444", {}),
+    (4096, 4096, 95, "422", {}),
+    (6000, 4000, 90, "420", {"restart_rows": 1}),
+    (1023, 769, 85, "422", {"restart_blocks": 5}),
+    (1001, 999, 80, "420", {}),
+], ids=["512_420", "1080p_420", "4096_444", "4096_422", "24MP_420_rst", "odd_422", "odd_420"])
+def test_full_size_against_oracle(w, h, q, sub, kw):
+    from paper_1311_5304_b200.block_transforms import alloc_pixels, render_rows
+    p, coeffs, qt = _synthetic(w, h, q, sub, **kw)
+    px = alloc_pixels(w, h)
+    render_rows(coeffs, qt, px, 0, coeffs.geometry.mcu_rows)
+    want = oracle.render(coeffs.y_blocks, coeffs.cb_blocks, coeffs.cr_blocks, qt, w, h,
+                         {"444": 0, "422": 1, "420": 2}[sub], True, threads=16)
+    assert np.array_equal(px.data, want)
+
+
+@pytest.mark.parametrize("sub", [0, 1, 2])
+def test_adversarial_coefficients(cuda, sub):
+    """Extreme int16 coefficients, q up to 255 (saturation on both ends),
+    sparse DC-only blocks and rounding-tie DC values."""
+    rng = np.random.default_rng(100 + sub)
+    w, h = 203, 77
+    mw, mh, ypm = {0: (8, 8, 1), 1: (16, 8, 2), 2: (16, 16, 4)}[sub]
+    mpr, rows = -(-w // mw), -(-h // mh)
+    n_c = mpr * rows
+    y = rng.integers(-32768, 32768, size=(n_c * ypm, 64)).astype(np.int16)
+    cb = rng.integers(-3000, 3000, size=(n_c, 64)).astype(np.int16)
+    cr = (rng.integers(-40, 40, size=(n_c, 64)) * (rng.random((n_c, 64)) < 0.2)).astype(np.int16)
+    cr[::3, 1:] = 0
+    cr[::3, 0] = rng.integers(-64, 64, size=len(cr[::3])) * 4 + 1  # DC-only, tie family
+    q = np.stack([rng.integers(1, 256, 64), rng.integers(1, 256, 64), np.full(64, 1)]).astype(np.int32)
+
+    class G:  # minimal golden-like record
+        pass
+    g = G()
+    g.sub, g.width, g.height, g.y, g.cb, g.cr, g.q = sub, w, h, y, cb, cr, q
+    for fast in (True, False):
+        got = _render(cuda, g, fast)
+        want = oracle.render(y, cb, cr, q, w, h, sub, fast)
+        assert np.array_equal(got, want)
+
+
+def test_device_batch_mixed_subsamplings(cuda):
+    from paper_1311_5304_b200 import device, entropy, parser
+    cases = [c for c in GOLDEN_CASES if c.width * c.height > 1000]
+    geos, coeffs = [], []
+    for c in cases:
+        p = parser.parse_stream(c.jpeg)
+        cf, _ = entropy.decode_all(p, c.jpeg)
+        geos.append(cf.geometry)
+        coeffs.append(cf)
+    batch = device.DeviceBatch(geos)
+    s = device.Stream()
+    for i, (c, cf) in enumerate(zip(cases, coeffs)):
+        batch.upload_coefficients(i, cf, s)
+        batch.upload_qtables(i, c.q, s)
+    batch.render(stream=s)
+    outs = [np.zeros((c.height, c.width, 3), np.uint8) for c in cases]
+    for i, o in enumerate(outs):
+        batch.download_rgb(i, o, s)
+    s.synchronize()
+    for c, o in zip(cases, outs):
+        assert np.array_equal(o, c.rgb), c.name
