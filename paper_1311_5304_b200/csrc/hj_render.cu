@@ -1,329 +1,491 @@
-// sm_100a kernels for the hetjpeg parallel phase:
-//   dequantise -> IDCT -> [h2v1 / h2v2 fancy upsample] -> YCbCr->RGB.
+// sm_100a render kernel: dequantise -> IDCT -> [h2v1 / h2v2 fancy upsample]
+// -> YCbCr->RGB, bit-exact against the reference's float64 path.
 //
-// Bit-exactness contract: the IDCT reproduces the reference's float64
-// operation sequence (kernels/_native.pyx:321-388, fallback.py:67-100)
-// with explicitly-rounded __dadd_rn/__dmul_rn (no FMA contraction), and the
-// colour conversion uses integer formulas proven equal to the reference's
-// float64 rounding over all 2^24 inputs (tools/gen_constants.py).
+// IDCT numerics:  every block is first transformed
+// in binary32 with the reference's AAN operation order, packed two columns /
+// two rows per f32x2 instruction (FFMA2/FADD2).  A rigorous first-order
+// error bound E = u * sum_i K_i |x_i| (K from tools/analysis/
+// screen_constants.py) brackets each sample; if no rounding boundary of
+// floor(s + 128.5) lies inside [s - E, s + E] for all 64 samples, the binary32
+// result provably rounds like the reference's float64 one.  Otherwise (a few
+// percent of real blocks, all blocks in "direct" mode) the block is queued and
+// recomputed in exact float64 (explicitly rounded __dadd_rn/__dmul_rn, the
+// reference's operation order) by the CTA's fallback pass.
 //
-// Work decomposition: one CTA of 128 threads owns a
-// strip of MCU columns of one image and sweeps down a range of MCU rows.
-// Each sweep step
-//   (1) IDCTs one MCU row of the strip, one 8x8 block per thread, entirely
-//       in registers (no transposes), into u8 sample planes in shared memory;
-//       4:2:2/4:2:0 also transform the chroma blocks of the MCU to the left
-//       and right of the strip (horizontal filter context), and 4:2:0 keeps a
-//       3-MCU-row chroma ring so the vertical context is transformed once;
-//   (2) upsamples + colour-converts from shared memory and stores
-//       interleaved RGB8 with 8-byte vector stores.
+// Work decomposition: a CTA (128 threads) owns a strip of MCU columns of one
+// image and sweeps down a range of MCU rows.  Per MCU row:
+//   (1) screen: each thread takes one job of two blocks (two Y blocks, or
+//       the Cb+Cr pair of one MCU), writes Y samples as u8 and chroma as SWAR
+//       words (Cb | Cr << 16) so the upsampler filters both planes per op;
+//   (2) exact fallback for queued blocks (float64, few threads);
+//   (3) upsample + colour + store: 8 pixels per item, integer colour
+//       formulas, saturating I2IP byte packing, 8-byte RGB stores.
+// 4:2:2 / 4:2:0 strips include the chroma MCU left/right of the strip; 4:2:0
+// keeps the previous / next chroma MCU row resident (vertical context).
 #include <cstdint>
 
+#include "hj_common.cuh"
 #include "hj_render.cuh"
-#include "hj_tables.h"
+#include "hj_screen.h"
 
 namespace hj {
 
 namespace {
 
-__constant__ double kPre[64] = HJ_PRESCALE_INIT;
-__constant__ double kBasis[64] = HJ_BASIS_INIT;
+__constant__ double kPre64[64] = HJ_PRESCALE_INIT;
+__constant__ double kBasis64[64] = HJ_BASIS_INIT;
+__constant__ float kScreenK[64] = HJ_SCREEN_K_INIT;
 
-// ---------------------------------------------------------------- float64
+typedef unsigned long long u64;
 
-__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
-
-// Exact int32 -> float64 without the (quarter-rate) I2F.F64 conversion:
-// as_double(0x43300000 : x ^ 0x80000000) == 2^52 + 2^31 + x.
-__device__ __forceinline__ double i2d(int x) {
-    return dsub(__hiloint2double(0x43300000, x ^ (int)0x80000000), 4503601774854144.0);
+// ---------------------------------------------------------- packed f32x2
+__device__ __forceinline__ u64 pk(float lo, float hi) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float plo(u64 v) {
+    float l, h;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(l), "=f"(h) : "l"(v));
+    return l;
+}
+__device__ __forceinline__ float phi(u64 v) {
+    float l, h;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(l), "=f"(h) : "l"(v));
+    return h;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+    u64 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+    u64 d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+    u64 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+    u64 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
 }
 
-// _round_u8(s + 128.0) (_native.pyx:312-318, 388): floor(fl(fl(s+128)+0.5))
-// clamped to [0,255].  fl(a+0.5) never changes floor() for |a| < 2^51, so
-// floor(fl(a+0.5)) = floor(a+0.5) is read off one round-down add into the
-// 0.5-spaced binade [2^51, 2^52): lo32(rd(a + 1.5*2^51 + 0.5)) = floor(2a+1).
-__device__ __forceinline__ int round_sample(double s) {
-    double a = dadd(s, 128.0);
-    double t = __dadd_rd(a, 3377699720527872.5);
-    int n = __double2loint(t) >> 1;
-    return min(max(n, 0), 255);
+// binary32 rotators (the reference's decimal literals, constants.py:31-35)
+#define F_SQRT2 1.414213562f
+#define F_ROT 1.847759065f
+#define F_ROT_P 1.082392200f
+#define F_ROT_M 2.613125930f
+
+// One AAN pass on 2 independent lanes, the node structure analysed by
+// tools/analysis/screen_constants.py: FFMA at tmp12 / t10 / t12, products at
+// t11 / z5, everything else one rounded add/sub.  tmp12 and t10 are carried
+// negated (exactly: round-to-nearest is sign-symmetric).
+__device__ __forceinline__ void aan_x2(u64 &d0, u64 &d1, u64 &d2, u64 &d3, u64 &d4, u64 &d5, u64 &d6,
+                                       u64 &d7) {
+    const u64 sq = pk(F_SQRT2, F_SQRT2), nsq = pk(-F_SQRT2, -F_SQRT2);
+    const u64 rot = pk(F_ROT, F_ROT), nrotp = pk(-F_ROT_P, -F_ROT_P), nrotm = pk(-F_ROT_M, -F_ROT_M);
+    u64 tmp10 = add2(d0, d4);
+    u64 tmp11 = sub2(d0, d4);
+    u64 tmp13 = add2(d2, d6);
+    u64 ntmp12 = fma2(sub2(d2, d6), nsq, tmp13);  // = -(a*SQRT2 - tmp13)
+    u64 e0 = add2(tmp10, tmp13);
+    u64 e3 = sub2(tmp10, tmp13);
+    u64 e1 = sub2(tmp11, ntmp12);
+    u64 e2 = add2(tmp11, ntmp12);
+    u64 z13 = add2(d5, d3);
+    u64 z10 = sub2(d5, d3);
+    u64 z11 = add2(d1, d7);
+    u64 z12 = sub2(d1, d7);
+    u64 t7 = add2(z11, z13);
+    u64 t11 = mul2(sub2(z11, z13), sq);
+    u64 z5 = mul2(add2(z10, z12), rot);
+    u64 nt10 = fma2(z12, nrotp, z5);  // = -(ROT_P*z12 - z5)
+    u64 t12 = fma2(z10, nrotm, z5);   // = -ROT_M*z10 + z5
+    u64 t6 = sub2(t12, t7);
+    u64 t5 = sub2(t11, t6);
+    u64 t4 = sub2(t5, nt10);
+    d0 = add2(e0, t7);
+    d1 = add2(e1, t6);
+    d2 = add2(e2, t5);
+    d3 = sub2(e3, t4);
+    d4 = add2(e3, t4);
+    d5 = sub2(e2, t5);
+    d6 = sub2(e1, t6);
+    d7 = sub2(e0, t7);
 }
 
-// One scaled-AAN 1-D pass, operation order of _native.pyx:321-351.
-__device__ __forceinline__ void aan8(double &x0, double &x1, double &x2, double &x3,
-                                     double &x4, double &x5, double &x6, double &x7) {
-    double tmp10 = dadd(x0, x4);
-    double tmp11 = dsub(x0, x4);
-    double tmp13 = dadd(x2, x6);
-    double tmp12 = dsub(dmul(dsub(x2, x6), HJ_SQRT2), tmp13);
-    double e0 = dadd(tmp10, tmp13);
-    double e3 = dsub(tmp10, tmp13);
-    double e1 = dadd(tmp11, tmp12);
-    double e2 = dsub(tmp11, tmp12);
-    double z13 = dadd(x5, x3);
-    double z10 = dsub(x5, x3);
-    double z11 = dadd(x1, x7);
-    double z12 = dsub(x1, x7);
-    double t7 = dadd(z11, z13);
-    double t11 = dmul(dsub(z11, z13), HJ_SQRT2);
-    double z5 = dmul(dadd(z10, z12), HJ_ROT);
-    double t10 = dsub(dmul(HJ_ROT_P, z12), z5);
-    double t12 = dadd(dmul(-HJ_ROT_M, z10), z5);
-    double t6 = dsub(t12, t7);
-    double t5 = dsub(t11, t6);
-    double t4 = dadd(t10, t5);
-    x0 = dadd(e0, t7);
-    x1 = dadd(e1, t6);
-    x2 = dadd(e2, t5);
-    x3 = dsub(e3, t4);
-    x4 = dadd(e3, t4);
-    x5 = dsub(e2, t5);
-    x6 = dsub(e1, t6);
-    x7 = dsub(e0, t7);
-}
-
-// One direct-basis 1-D pass (_native.pyx:354-361): y[k] = sum_r T[r][k]*x[r],
-// accumulated from 0.0 in ascending r.
-__device__ __forceinline__ void direct8(double *x) {
-    double y[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        double acc = 0.0;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) acc = dadd(acc, dmul(kBasis[r * 8 + k], x[r]));
-        y[k] = acc;
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = y[k];
-}
-
-__device__ __forceinline__ int coef_at(const int4 (&raw)[8], int r, int c) {
-    int w = (c >> 1) == 0 ? raw[r].x : (c >> 1) == 1 ? raw[r].y : (c >> 1) == 2 ? raw[r].z : raw[r].w;
-    return (c & 1) ? (w >> 16) : (int)(short)(w & 0xffff);
-}
-
-// Shared-memory int4 load that the compiler may not hoist out of the
-// block loop (a hoisted q table would pin 64 registers for the whole sweep).
-__device__ __forceinline__ int4 lds128_volatile(const int *p) {
-    int4 v;
+__device__ __forceinline__ float4 lds128f(const float *p) {
+    float4 v;
     unsigned a = (unsigned)__cvta_generic_to_shared(p);
-    asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
     return v;
 }
 
-// Pre-rounding float64 core of one block of dequantised coefficients
-// dq[64] (natural order).  Result in g[64].
-template <bool DIRECT>
-__device__ __forceinline__ void idct_core(const int (&dq)[64], double (&g)[64]) {
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        double d[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            int v = dq[r * 8 + c];
-            d[r] = DIRECT ? i2d(v) : dmul(i2d(v), kPre[r * 8 + c]);
-        }
-        if (DIRECT) {
-            direct8(d);
-        } else {
-            aan8(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7]);
-        }
-#pragma unroll
-        for (int r = 0; r < 8; ++r) g[r * 8 + c] = d[r];
-    }
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        double *x = &g[r * 8];
-        if (DIRECT) {
-            direct8(x);
-        } else {
-            aan8(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
-        }
-    }
+// Per-sample rounding test of one f32x2 output pair.  t = v + C, C = 3200.5 -/+ Eq
+// lands in the binade [2048, 4096) (ulp 2^-12) for v in [-200, 895]: integer
+// part floor(v + 128.5) = (bits >> 12) - 0x45400.  `acc` collects
+// bits(t-) ^ bits(t+): any bit >= 12 means some bracket crosses a boundary.
+// v > 895 gives t >= 4096, n >= 1024 and a saturated 255 (correct: the true
+// sample exceeds 255.5); v < -200 is clamped (its output is 0 either way).
+__device__ __forceinline__ void round_pair(u64 v, u64 cm, u64 cp, uint32_t &acc, int &n_lo, int &n_hi) {
+    float lo = fmaxf(plo(v), -200.0f), hi = fmaxf(phi(v), -200.0f);
+    u64 w = pk(lo, hi);
+    u64 tm = add2(w, cm), tp = add2(w, cp);
+    uint32_t a0 = __float_as_uint(plo(tm)), a1 = __float_as_uint(phi(tm));
+    uint32_t b0 = __float_as_uint(plo(tp)), b1 = __float_as_uint(phi(tp));
+    acc |= (a0 ^ b0) | (a1 ^ b1);
+    n_lo = (int)(a0 >> 12) - 0x45400;
+    n_hi = (int)(a1 >> 12) - 0x45400;
 }
 
-// Dequantise + IDCT + round one block (global) into an 8x8 window of a u8
-// plane in shared memory (row stride `stride`, 8-byte aligned).
-template <bool DIRECT>
-__device__ __noinline__ void idct_block(const int16_t *__restrict__ src, const int *q,
-                                           uint8_t *dst, int stride) {
+// FP32 screen of one block: returns true (and the 64 samples, u8 row-major,
+// 4 per word) when every sample is proven equal to the reference's float64
+// result; false = recompute exactly.
+__device__ __forceinline__ bool screen_block(const int16_t *__restrict__ src, const float *qf,
+                                             uint32_t (&out)[16]) {
     int4 raw[8];
     const int4 *s4 = reinterpret_cast<const int4 *>(src);
 #pragma unroll
     for (int r = 0; r < 8; ++r) raw[r] = __ldg(s4 + r);
-    int dq[64];  // dequantise: int16 coefficient * qtable entry (fallback.py:194-195)
+    u64 X[4][8];  // X[cp][r] = (x[r][2cp], x[r][2cp+1])
+    float b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-        int4 q0 = lds128_volatile(q + r * 8), q1 = lds128_volatile(q + r * 8 + 4);
-        const int qa[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        float4 qa = lds128f(qf + r * 8), qb = lds128f(qf + r * 8 + 4);
+        const int w[4] = {raw[r].x, raw[r].y, raw[r].z, raw[r].w};
+        const float q[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
 #pragma unroll
-        for (int c = 0; c < 8; ++c) dq[r * 8 + c] = coef_at(raw, r, c) * qa[c];
+        for (int cp = 0; cp < 4; ++cp) {
+            float c0 = (float)(short)(w[cp] & 0xffff);
+            float c1 = (float)(w[cp] >> 16);
+            u64 x = mul2(pk(c0, c1), pk(q[2 * cp], q[2 * cp + 1]));
+            X[cp][r] = x;
+            if (cp & 1) {
+                b1 = fmaf(fabsf(plo(x)), kScreenK[r * 8 + 2 * cp], b1);
+                b3 = fmaf(fabsf(phi(x)), kScreenK[r * 8 + 2 * cp + 1], b3);
+            } else {
+                b0 = fmaf(fabsf(plo(x)), kScreenK[r * 8 + 2 * cp], b0);
+                b2 = fmaf(fabsf(phi(x)), kScreenK[r * 8 + 2 * cp + 1], b2);
+            }
+        }
     }
-    double g[64];
-    idct_core<DIRECT>(dq, g);
+    // bound: E = u*B*(1+2e-3) + 2^-13 (t rounding) + 2^-30 (float64 side),
+    // rounded up to the 2^-12 grid so 3200.5 +- Eq is exact in binary32
+    float B = (b0 + b1) + (b2 + b3);
+    float e = fmaf(B, 5.972e-8f, 1.2208e-4f);
+    float eq = ceilf(e * 4096.0f) * (1.0f / 4096.0f);
+    u64 cm = pk(3200.5f - eq, 3200.5f - eq), cpl = pk(3200.5f + eq, 3200.5f + eq);
+
 #pragma unroll
+    for (int cp = 0; cp < 4; ++cp)
+        aan_x2(X[cp][0], X[cp][1], X[cp][2], X[cp][3], X[cp][4], X[cp][5], X[cp][6], X[cp][7]);
+
+    uint32_t acc = 0;
+#pragma unroll
+    for (int rp = 0; rp < 4; ++rp) {
+        const int r0 = 2 * rp, r1 = 2 * rp + 1;
+        u64 Q[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            u64 a = X[j >> 1][r0], b = X[j >> 1][r1];
+            Q[j] = (j & 1) ? pk(phi(a), phi(b)) : pk(plo(a), plo(b));
+        }
+        aan_x2(Q[0], Q[1], Q[2], Q[3], Q[4], Q[5], Q[6], Q[7]);
+        int n0[8], n1[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) round_pair(Q[c], cm, cpl, acc, n0[c], n1[c]);
+        out[r0 * 2] = pack4(n0[0], n0[1], n0[2], n0[3]);
+        out[r0 * 2 + 1] = pack4(n0[4], n0[5], n0[6], n0[7]);
+        out[r1 * 2] = pack4(n1[0], n1[1], n1[2], n1[3]);
+        out[r1 * 2 + 1] = pack4(n1[4], n1[5], n1[6], n1[7]);
+    }
+    return (acc >> 12) == 0;
+}
+
+// ------------------------------------------------------ exact fallback
+
+// float64 IDCT of one block in the reference's exact operation order
+// (_native.pyx:364-388), column-pass results staged in shared memory
+// (`g`, 64 doubles) so the register footprint stays small.  Writes the 64
+// rounded samples (u8, row-major, 4 per word) to `out` (shared, 64 bytes).
+__device__ __noinline__ void exact_block(const int16_t *__restrict__ src, const int *q, bool direct,
+                                         double *g, uint32_t *out) {
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+        double d[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            int v = (int)src[r * 8 + c] * q[r * 8 + c];
+            d[r] = direct ? i2d(v) : dmul(i2d(v), kPre64[r * 8 + c]);
+        }
+        if (direct) direct8(d, kBasis64);
+        else aan8(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7]);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) g[r * 8 + c] = d[r];
+    }
+#pragma unroll 1
     for (int r = 0; r < 8; ++r) {
-        uint32_t lo = 0, hi = 0;
+        double x[8];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) lo |= (uint32_t)round_sample(g[r * 8 + c]) << (8 * c);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) hi |= (uint32_t)round_sample(g[r * 8 + 4 + c]) << (8 * c);
-        *reinterpret_cast<uint2 *>(dst + r * stride) = make_uint2(lo, hi);
+        for (int k = 0; k < 8; ++k) x[k] = g[r * 8 + k];
+        if (direct) direct8(x, kBasis64);
+        else aan8(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
+        out[2 * r] = pack4(round_sample(x[0]), round_sample(x[1]), round_sample(x[2]), round_sample(x[3]));
+        out[2 * r + 1] = pack4(round_sample(x[4]), round_sample(x[5]), round_sample(x[6]), round_sample(x[7]));
     }
 }
 
-// ---------------------------------------------------------------- colour
-
-// Integer forms of _color_px (_native.pyx:391-395), exhaustively verified
-// (tools/gen_constants.py colour_constants).  Returns 0x00BBGGRR.
-__device__ __forceinline__ uint32_t colour(int y, int cb, int cr) {
-    int yk = y << HJ_COL_K;
-    int r = (yk + HJ_COL_AR * cr + HJ_COL_CR) >> HJ_COL_K;
-    int g = (yk + HJ_COL_AGB * cb + HJ_COL_AGR * cr + HJ_COL_CG) >> HJ_COL_K;
-    int b = (yk + HJ_COL_AB * cb + HJ_COL_CB) >> HJ_COL_K;
-    // the one float64 tie whose offset depends on Y
-    if (cb == 78 && cr == 178 && (unsigned)(y - 47) <= 35u) g -= 1;
-    r = min(max(r, 0), 255);
-    g = min(max(g, 0), 255);
-    b = min(max(b, 0), 255);
-    return (uint32_t)r | ((uint32_t)g << 8) | ((uint32_t)b << 16);
-}
-
-// Store 8 pixels (packed 0x00BBGGRR each) as 24 interleaved bytes at
-// rgb + off, cropping to `npx` pixels.
-__device__ __forceinline__ void store8(uint8_t *__restrict__ dst, const uint32_t (&px)[8], int npx) {
-    uint32_t w[6];
-    w[0] = px[0] | (px[1] << 24);
-    w[1] = (px[1] >> 8) | (px[2] << 16);
-    w[2] = (px[2] >> 16) | (px[3] << 8);
-    w[3] = px[4] | (px[5] << 24);
-    w[4] = (px[5] >> 8) | (px[6] << 16);
-    w[5] = (px[6] >> 16) | (px[7] << 8);
-    uintptr_t a = reinterpret_cast<uintptr_t>(dst);
-    if (npx == 8 && (a & 7) == 0) {
-        uint2 *d = reinterpret_cast<uint2 *>(dst);
-        d[0] = make_uint2(w[0], w[1]);
-        d[1] = make_uint2(w[2], w[3]);
-        d[2] = make_uint2(w[4], w[5]);
-    } else if (npx == 8 && (a & 3) == 0) {
-        uint32_t *d = reinterpret_cast<uint32_t *>(dst);
-#pragma unroll
-        for (int i = 0; i < 6; ++i) d[i] = w[i];
-    } else {
-        for (int i = 0; i < npx * 3; ++i) dst[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
-    }
-}
-
-// ---------------------------------------------------------------- kernel
+// ------------------------------------------------------------- geometry
 
 template <int SUB>
 struct Geo;
 template <>
 struct Geo<HJ_SUB_444> {
     static constexpr int S = kStrip444, YPM = 1, MW = 8, MH = 8;
-    static constexpr int YW = 8 * S, CW = 8 * S, CROWS = 8;
+    static constexpr int YW = 8 * S;   // Y plane width (bytes)
+    static constexpr int CW = 8 * S;   // chroma window width (words)
+    static constexpr int CROWS = 8;
 };
 template <>
 struct Geo<HJ_SUB_422> {
     static constexpr int S = kStrip422, YPM = 2, MW = 16, MH = 8;
-    static constexpr int YW = 16 * S, CW = 8 * (S + 2), CROWS = 8;
+    static constexpr int YW = 16 * S;
+    static constexpr int CW = 8 * (S + 2);
+    static constexpr int CROWS = 8;
 };
 template <>
 struct Geo<HJ_SUB_420> {
     static constexpr int S = kStrip420, YPM = 4, MW = 16, MH = 16;
-    static constexpr int YW = 16 * S, CW = 8 * (S + 2), CROWS = 24;  // 3-row ring
+    static constexpr int YW = 16 * S;
+    static constexpr int CW = 8 * (S + 2);
+    static constexpr int CROWS = 17;  // MCU rows r, r+1 (8 rows each) + last row of r-1
 };
 
-template <int SUB, bool DIRECT>
-__global__ void __launch_bounds__(kThreads, 2)
+#ifndef HJ_MIN_CTAS
+#define HJ_MIN_CTAS 4
+#endif
+constexpr int kFallbackSlots = 8;    // concurrent exact-fallback jobs per CTA
+constexpr int kQueueMax = 256;  // >= blocks of one sweep step
+
+template <int SUB>
+struct Smem {
+    using G = Geo<SUB>;
+    uint8_t ys[G::MH * G::YW];
+    uint32_t cs[G::CROWS * G::CW];          // SWAR chroma: Cb | Cr << 16
+    float qf[3][64];                        // binary32 q * pre (screen)
+    int qi[3][64];                          // integer q (exact path)
+    double g[kFallbackSlots][64];           // exact-path column results
+    uint32_t fout[kFallbackSlots][16];      // exact-path samples
+    uint32_t queue[kQueueMax];              // fallback jobs
+    uint32_t qdst[kQueueMax];
+    uint4 cscratch[kThreads][4];            // Cb samples of a chroma job
+    int n_queue;
+};
+
+__device__ __forceinline__ void write_y_rows(uint8_t *ys, int yoff, int stride, const uint32_t (&w)[16]) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+        *reinterpret_cast<uint2 *>(ys + yoff + r * stride) = make_uint2(w[2 * r], w[2 * r + 1]);
+}
+
+// Interleave Cb and Cr sample rows into SWAR words: word k = cb_k | cr_k << 16.
+__device__ __forceinline__ void write_c_rows(uint32_t *cs, int coff, int stride, const uint32_t (&cb)[16],
+                                             const uint32_t (&cr)[16]) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t a = cb[2 * r + h], b = cr[2 * r + h];
+            uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+            uint4 v = make_uint4(__byte_perm(t0, 0, 0x4140), __byte_perm(t0, 0, 0x4342),
+                                 __byte_perm(t1, 0, 0x4140), __byte_perm(t1, 0, 0x4342));
+            *reinterpret_cast<uint4 *>(cs + coff + r * stride + 4 * h) = v;
+        }
+    }
+}
+
+template <int SUB>
+__global__ void __launch_bounds__(kThreads, HJ_MIN_CTAS)
 render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ tiles) {
     using G = Geo<SUB>;
-    __shared__ __align__(16) uint8_t ys[G::MH * G::YW];
-    __shared__ __align__(16) uint8_t cbs[G::CROWS * G::CW];
-    __shared__ __align__(16) uint8_t crs[G::CROWS * G::CW];
-    __shared__ __align__(16) int qs[3 * 64];
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    Smem<SUB> &sm = *reinterpret_cast<Smem<SUB> *>(smem_raw);
 
     const Tile t = tiles[blockIdx.x];
     const hj_image_t im = images[t.image];
     const int tid = threadIdx.x;
     const int mpr = im.mcus_per_row;
     const int S = t.m1 - t.m0;
-    for (int i = tid; i < 192; i += kThreads) qs[i] = im.q[i];
+    const bool direct = (im.flags & HJ_FLAG_DIRECT_IDCT) != 0;
+    for (int i = tid; i < 192; i += kThreads) {
+        int q = im.q[i];
+        sm.qi[i >> 6][i & 63] = q;
+        sm.qf[i >> 6][i & 63] = (float)((double)q * kPre64[i & 63]);
+    }
+    if (tid == 0) sm.n_queue = 0;
 
     // chroma MCU window of the strip: [m0-1, m1+1) for 4:2:2/4:2:0
     const int cm_lo = (SUB == HJ_SUB_444) ? t.m0 : t.m0 - 1;
     const int n_cm = (SUB == HJ_SUB_444) ? S : S + 2;
+    // Y jobs: two blocks each (444: MCU pair; 422: one MCU; 420: half MCU)
+    const int n_yj = (SUB == HJ_SUB_444) ? (S + 1) / 2 : (SUB == HJ_SUB_422 ? S : 2 * S);
     __syncthreads();
 
-    // Resolve chroma job j of MCU row `row` (j in [0, 2*n_cm): component
-    // j / n_cm, window MCU j % n_cm) to its source block and plane window.
-    auto chroma_job = [&](int row, int slot, int j, const int16_t *&src, const int *&q,
-                          uint8_t *&dst) -> bool {
-        int comp = j / n_cm, lm = j - comp * n_cm;
-        int m = cm_lo + lm;
-        if (m < 0 || m >= mpr) return false;
-        src = (comp == 0 ? im.cb : im.cr) + ((int64_t)row * mpr + m) * 64;
-        q = qs + 64 * (1 + comp);
-        dst = (comp == 0 ? cbs : crs) + slot * 8 * G::CW + lm * 8;
-        return true;
+    auto enqueue = [&](uint32_t job, uint32_t dst) {
+        int k = atomicAdd(&sm.n_queue, 1);
+        if (k < kQueueMax) {
+            sm.queue[k] = job;
+            sm.qdst[k] = dst;
+        }
     };
 
-    if (SUB == HJ_SUB_420) {
-        // prime the ring with MCU rows r0-1 (if any) and r0
-        int pre_lo = t.r0 > 0 ? t.r0 - 1 : t.r0;
-        int n_pre = (t.r0 - pre_lo + 1) * 2 * n_cm;
+    // One transform job: two blocks.  Y job: blocks side by side in the Y
+    // plane; chroma job: the Cb and Cr block of one MCU into SWAR words.
+    // Queue entry: comp << 30 | block index; destination: Y byte offset, or
+    // 1 << 31 | lane << 30 | chroma word offset.
+    auto run_job = [&](int job, int row, int cslot) {
+        if (job < n_yj) {
+            // Y block k of the job: 444 MCUs 2j, 2j+1; 422 MCU j (left,
+            // right); 420 MCU j/2, blocks 0,1 (top) or 2,3 (bottom)
+            const int nb = (SUB == HJ_SUB_444 && 2 * job + 1 >= S) ? 1 : 2;
 #pragma unroll 1
-        for (int j = tid; j < n_pre; j += kThreads) {
-            int rr = pre_lo + j / (2 * n_cm);
-            const int16_t *src;
-            const int *q;
-            uint8_t *dst;
-            if (chroma_job(rr, rr % 3, j % (2 * n_cm), src, q, dst)) idct_block<DIRECT>(src, q, dst, G::CW);
+            for (int k = 0; k < nb; ++k) {
+                int64_t blk;
+                int yoff;
+                if (SUB == HJ_SUB_444) {
+                    blk = (int64_t)row * mpr + t.m0 + 2 * job + k;
+                    yoff = (2 * job + k) * 8;
+                } else if (SUB == HJ_SUB_422) {
+                    blk = ((int64_t)row * mpr + t.m0 + job) * 2 + k;
+                    yoff = job * 16 + k * 8;
+                } else {
+                    int lm = job >> 1, half = job & 1;
+                    blk = ((int64_t)row * mpr + t.m0 + lm) * 4 + 2 * half + k;
+                    yoff = half * 8 * G::YW + lm * 16 + k * 8;
+                }
+                uint32_t w[16];
+                bool ok = !direct && screen_block(im.y + blk * 64, sm.qf[0], w);
+                if (ok) write_y_rows(sm.ys, yoff, G::YW, w);
+                else enqueue((uint32_t)blk, (uint32_t)yoff);
+            }
+        } else {
+            int lm = job - n_yj;
+            int m = cm_lo + lm;
+            if (m < 0 || m >= mpr) return;
+            int64_t blk = (int64_t)row * mpr + m;
+            int coff = cslot * 8 * G::CW + lm * 8;
+            bool okb, okr;
+            {
+                uint32_t wb[16];
+                okb = !direct && screen_block(im.cb + blk * 64, sm.qf[1], wb);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    sm.cscratch[tid][i] = make_uint4(wb[4 * i], wb[4 * i + 1], wb[4 * i + 2], wb[4 * i + 3]);
+            }
+            uint32_t wr[16];
+            okr = !direct && screen_block(im.cr + blk * 64, sm.qf[2], wr);
+            if (okb && okr) {
+                uint32_t wb[16];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    uint4 v = sm.cscratch[tid][i];
+                    wb[4 * i] = v.x;
+                    wb[4 * i + 1] = v.y;
+                    wb[4 * i + 2] = v.z;
+                    wb[4 * i + 3] = v.w;
+                }
+                write_c_rows(sm.cs, coff, G::CW, wb, wr);
+            } else {
+                // the exact path writes both 16-bit lanes of this MCU's words
+                enqueue((uint32_t)blk | (1u << 30), (uint32_t)coff | (1u << 31));
+                enqueue((uint32_t)blk | (2u << 30), (uint32_t)coff | (1u << 31) | (1u << 30));
+            }
         }
+    };
+
+    auto fallback_pass = [&]() {
+        __syncthreads();
+        const int n = min(sm.n_queue, kQueueMax);
+        if (tid < kFallbackSlots) {
+            for (int e = tid; e < n; e += kFallbackSlots) {
+                uint32_t job = sm.queue[e], dst = sm.qdst[e];
+                int comp = job >> 30;
+                int64_t blk = job & 0x3fffffff;
+                const int16_t *src = (comp == 0 ? im.y : comp == 1 ? im.cb : im.cr) + blk * 64;
+                exact_block(src, sm.qi[comp], direct, sm.g[tid], sm.fout[tid]);
+                const uint32_t *o = sm.fout[tid];
+                if (!(dst >> 31)) {
+                    for (int r = 0; r < 8; ++r)
+                        *reinterpret_cast<uint2 *>(sm.ys + dst + r * G::YW) = make_uint2(o[2 * r], o[2 * r + 1]);
+                } else {
+                    int coff = dst & 0x3fffffff, lane = (dst >> 30) & 1;
+                    uint16_t *cs16 = reinterpret_cast<uint16_t *>(sm.cs);
+                    const uint8_t *ob = reinterpret_cast<const uint8_t *>(o);
+                    for (int r = 0; r < 8; ++r)
+                        for (int c = 0; c < 8; ++c) cs16[2 * (coff + r * G::CW + c) + lane] = ob[r * 8 + c];
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) sm.n_queue = 0;
+    };
+
+    // edge replication of the padded chroma plane at the image's left/right
+    // edge (fallback.py:200-212 / _native.pyx:477-480 edge copy)
+    auto edge_fix = [&](int cslot) {
+        if (SUB == HJ_SUB_444) return;
+        for (int r = tid; r < 16; r += kThreads) {
+            uint32_t *row = sm.cs + (cslot * 8 + (r & 7)) * G::CW;
+            if (r < 8 && t.m0 == 0) row[7] = row[8];
+            if (r >= 8 && t.m1 == mpr) row[8 * (S + 1)] = row[8 * (S + 1) - 1];
+        }
+    };
+
+    // 4:2:0 chroma rows: MCU row rr lives in slot rr & 1 (rows 0-7 / 8-15);
+    // row 16 keeps sample row 7 of MCU row r-1 (the filter's upper context).
+    auto save_prev_last = [&](int rr) {
+        const uint32_t *src = sm.cs + ((rr & 1) * 8 + 7) * G::CW;
+        for (int i = tid; i < G::CW; i += kThreads) sm.cs[16 * G::CW + i] = src[i];
+    };
+    if (SUB == HJ_SUB_420) {
+        if (t.r0 > 0) {  // transform MCU row r0-1 and keep its last sample row
+            for (int j = tid; j < n_cm; j += kThreads) run_job(n_yj + j, t.r0 - 1, (t.r0 - 1) & 1);
+            fallback_pass();
+            edge_fix((t.r0 - 1) & 1);
+            __syncthreads();
+            save_prev_last(t.r0 - 1);
+            __syncthreads();
+        }
+        for (int j = tid; j < n_cm; j += kThreads) run_job(n_yj + j, t.r0, t.r0 & 1);
+        fallback_pass();
+        edge_fix(t.r0 & 1);
     }
 
 #pragma unroll 1
     for (int row = t.r0; row < t.r1; ++row) {
-        // ---- (1) transforms of this step
-        const int n_y = G::YPM * S;
-        int n_c = 0, c_row = row;
+        // ---- (1) screen transforms of this step
+        int c_row = row, n_c = n_cm;
         if (SUB == HJ_SUB_420) {
             c_row = row + 1;
-            n_c = (c_row < im.mcu_rows) ? 2 * n_cm : 0;
-        } else {
-            n_c = 2 * n_cm;
+            n_c = (c_row < im.mcu_rows) ? n_cm : 0;
         }
+        const int cslot = (SUB == HJ_SUB_420) ? (c_row & 1) : 0;
 #pragma unroll 1
-        for (int j = tid; j < n_y + n_c; j += kThreads) {
-            const int16_t *src;
-            const int *q;
-            uint8_t *dst;
-            int stride;
-            if (j < n_y) {
-                int lm = j / G::YPM, b = j - lm * G::YPM;
-                int64_t blk = ((int64_t)row * mpr + t.m0 + lm) * G::YPM + b;
-                // Y block b of the MCU: 4:2:2 left/right, 4:2:0 raster 2x2
-                int bx = (G::YPM == 1) ? 0 : (b & 1), by = (G::YPM == 4) ? (b >> 1) : 0;
-                src = im.y + blk * 64;
-                q = qs;
-                dst = ys + by * 8 * G::YW + (lm * (G::MW / 8) + bx) * 8;
-                stride = G::YW;
-            } else {
-                if (!chroma_job(c_row, SUB == HJ_SUB_420 ? c_row % 3 : 0, j - n_y, src, q, dst)) continue;
-                stride = G::CW;
-            }
-            idct_block<DIRECT>(src, q, dst, stride);
-        }
+        for (int j = tid; j < n_yj + n_c; j += kThreads) run_job(j, row, cslot);
+        // ---- (2) exact fallback
+        fallback_pass();
+        if (n_c) edge_fix(cslot);
         __syncthreads();
 
-        // ---- (2) upsample + colour + store
+        // ---- (3) upsample + colour + store
         const int y_base = row * G::MH;
-        const int n_groups = (G::MW / 8) * S;  // 8-pixel groups per pixel row
+        const int n_groups = (G::MW / 8) * S;
         const int x_base = t.m0 * G::MW;
-        const int cw_img = 8 * mpr;            // padded chroma plane width
 #pragma unroll 1
         for (int it = tid; it < G::MH * n_groups; it += kThreads) {
             int oy = it / n_groups, gx = it - oy * n_groups;
@@ -331,163 +493,123 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
             int x0 = x_base + gx * 8;
             int npx = min(8, im.width - x0);
             if (y >= im.height || npx <= 0) continue;
-            const uint8_t *yrow = ys + oy * G::YW + gx * 8;
-            uint32_t px[8];
+            uint2 yv = *reinterpret_cast<const uint2 *>(sm.ys + oy * G::YW + gx * 8);
+            int Y[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                Y[i] = (yv.x >> (8 * i)) & 0xff;
+                Y[4 + i] = (yv.y >> (8 * i)) & 0xff;
+            }
+            int cbv[8], crv[8];
             if (SUB == HJ_SUB_444) {
-                const uint8_t *cbr = cbs + oy * G::CW + gx * 8;
-                const uint8_t *crr = crs + oy * G::CW + gx * 8;
+                const uint32_t *cr = sm.cs + oy * G::CW + gx * 8;
+                uint4 a = *reinterpret_cast<const uint4 *>(cr), b = *reinterpret_cast<const uint4 *>(cr + 4);
+                const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-                for (int i = 0; i < 8; ++i) px[i] = colour(yrow[i], cbr[i], crr[i]);
+                for (int i = 0; i < 8; ++i) {
+                    cbv[i] = w[i] & 0xff;
+                    crv[i] = w[i] >> 16;
+                }
             } else {
-                // chroma samples k0-1 .. k0+4 of this group, clamped to the
-                // padded plane (edge copy), as window-local columns
-                const int k0 = 8 * t.m0 + 4 * gx;
-                int cb_s[6], cr_s[6];
+                // window-local chroma column of sample k0 = 8*m0 + 4*gx
+                const int kl = 8 * (t.m0 - cm_lo) + 4 * gx;
+                uint32_t c[6];
                 if (SUB == HJ_SUB_422) {
-                    const uint8_t *cbr = cbs + oy * G::CW;
-                    const uint8_t *crr = crs + oy * G::CW;
-#pragma unroll
-                    for (int i = 0; i < 6; ++i) {
-                        int k = min(max(k0 - 1 + i, 0), cw_img - 1) - 8 * cm_lo;
-                        cb_s[i] = cbr[k];
-                        cr_s[i] = crr[k];
-                    }
+                    const uint32_t *cr = sm.cs + oy * G::CW + kl;
+                    uint4 mid = *reinterpret_cast<const uint4 *>(cr);
+                    c[0] = cr[-1];
+                    c[1] = mid.x;
+                    c[2] = mid.y;
+                    c[3] = mid.z;
+                    c[4] = mid.w;
+                    c[5] = cr[4];
+                    // h2v1: even (3c+prev+1)>>2, odd (3c+next+2)>>2 per 16-bit lane
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        int cb3 = 3 * cb_s[i + 1], cr3 = 3 * cr_s[i + 1];
-                        px[2 * i] = colour(yrow[2 * i], (cb3 + cb_s[i] + 1) >> 2, (cr3 + cr_s[i] + 1) >> 2);
-                        px[2 * i + 1] = colour(yrow[2 * i + 1], (cb3 + cb_s[i + 2] + 2) >> 2,
-                                               (cr3 + cr_s[i + 2] + 2) >> 2);
+                        uint32_t t3 = c[i + 1] * 3u + 0x00010001u;
+                        uint32_t ev = t3 + c[i], od = t3 + c[i + 2] + 0x00010001u;
+                        cbv[2 * i] = (ev >> 2) & 0xff;
+                        crv[2 * i] = ev >> 18;
+                        cbv[2 * i + 1] = (od >> 2) & 0xff;
+                        crv[2 * i + 1] = od >> 18;
                     }
                 } else {
                     const int ch_img = 8 * im.mcu_rows;
                     int ci = 8 * row + (oy >> 1);
                     int cf = min(max(ci + ((oy & 1) ? 1 : -1), 0), ch_img - 1);
-                    const int on = ((ci >> 3) % 3) * 8 + (ci & 7);
-                    const int of = ((cf >> 3) % 3) * 8 + (cf & 7);
-                    const uint8_t *cbn = cbs + on * G::CW, *cbf = cbs + of * G::CW;
-                    const uint8_t *crn = crs + on * G::CW, *crf = crs + of * G::CW;
-#pragma unroll
-                    for (int i = 0; i < 6; ++i) {
-                        int k = min(max(k0 - 1 + i, 0), cw_img - 1) - 8 * cm_lo;
-                        cb_s[i] = 3 * cbn[k] + cbf[k];
-                        cr_s[i] = 3 * crn[k] + crf[k];
-                    }
+                    // sample row -> smem row: MCU row r in slot r&1, r+1 in the other,
+                    // row 8r-1 in the saved row 16
+                    const int rn = (row & 1) * 8 + (ci & 7);
+                    const int rf = cf < 8 * row ? 16 : (((cf >> 3) & 1) * 8 + (cf & 7));
+                    const uint32_t *cn = sm.cs + rn * G::CW + kl;
+                    const uint32_t *cfp = sm.cs + rf * G::CW + kl;
+                    uint4 mn = *reinterpret_cast<const uint4 *>(cn), mf = *reinterpret_cast<const uint4 *>(cfp);
+                    // colsum = 3*near + far per lane (libjpeg h2v2 fancy)
+                    c[0] = cn[-1] * 3u + cfp[-1];
+                    c[1] = mn.x * 3u + mf.x;
+                    c[2] = mn.y * 3u + mf.y;
+                    c[3] = mn.z * 3u + mf.z;
+                    c[4] = mn.w * 3u + mf.w;
+                    c[5] = cn[4] * 3u + cfp[4];
+                    // even (3cs+prev+8)>>4, odd (3cs+next+7)>>4
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        int cb3 = 3 * cb_s[i + 1], cr3 = 3 * cr_s[i + 1];
-                        px[2 * i] = colour(yrow[2 * i], (cb3 + cb_s[i] + 8) >> 4, (cr3 + cr_s[i] + 8) >> 4);
-                        px[2 * i + 1] = colour(yrow[2 * i + 1], (cb3 + cb_s[i + 2] + 7) >> 4,
-                                               (cr3 + cr_s[i + 2] + 7) >> 4);
+                        uint32_t t3 = c[i + 1] * 3u + 0x00080008u;
+                        uint32_t ev = t3 + c[i], od = t3 + c[i + 2] - 0x00010001u;
+                        cbv[2 * i] = (ev >> 4) & 0xff;
+                        crv[2 * i] = ev >> 20;
+                        cbv[2 * i + 1] = (od >> 4) & 0xff;
+                        crv[2 * i + 1] = od >> 20;
                     }
                 }
             }
-            store8(im.rgb + ((int64_t)y * im.width + x0) * 3, px, npx);
+            Rgb p[8];
+            bool special = false;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) p[i] = colour(Y[i], cbv[i], crv[i], special);
+            if (special) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) p[i].g = colour_g_exact(Y[i], cbv[i], crv[i]);
+            }
+            uint32_t w[6];
+            pack_rgb8(p, w);
+            store_rgb8(im.rgb + ((int64_t)y * im.width + x0) * 3, w, npx);
         }
         __syncthreads();
+        if (SUB == HJ_SUB_420 && row + 1 < t.r1) {
+            save_prev_last(row);
+            __syncthreads();
+        }
     }
 }
 
-// ------------------------------------------------------- per-block kernels
-
-template <bool DIRECT>
-__global__ void idct_blocks_kernel(const int32_t *__restrict__ deq, int64_t n,
-                                   uint8_t *__restrict__ out, double *__restrict__ out_f64) {
-    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (b >= n) return;
-    // reuse the block core with q == 1 over the int32 input split in halves:
-    // the dequantised product is passed through an int4 view per row.
-    int dq[64];
-    const int4 *src = reinterpret_cast<const int4 *>(deq + b * 64);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        int4 v = src[i];
-        dq[4 * i] = v.x;
-        dq[4 * i + 1] = v.y;
-        dq[4 * i + 2] = v.z;
-        dq[4 * i + 3] = v.w;
+template <int SUB>
+cudaError_t launch_sub(const hj_image_t *images, const Tile *tiles, int n_tiles, cudaStream_t stream) {
+    static bool configured = false;
+    const int bytes = (int)sizeof(Smem<SUB>);
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(render_kernel<SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              bytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
     }
-    double g[64];
-    idct_core<DIRECT>(dq, g);
-    if (out_f64) {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) out_f64[b * 64 + i] = g[i];
-    } else {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) out[b * 64 + i] = (uint8_t)round_sample(g[i]);
-    }
-}
-
-__global__ void ycbcr_kernel(const uint8_t *__restrict__ y, const uint8_t *__restrict__ cb,
-                             const uint8_t *__restrict__ cr, uint8_t *__restrict__ rgb, int64_t n) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    uint32_t p = colour(y[i], cb[i], cr[i]);
-    rgb[3 * i] = (uint8_t)p;
-    rgb[3 * i + 1] = (uint8_t)(p >> 8);
-    rgb[3 * i + 2] = (uint8_t)(p >> 16);
-}
-
-// Algorithm 1 on one 8-sample row, floor division:
-// out[2k] = (3s[k] + s[k-1] + 1) / 4, out[2k+1] = (3s[k] + s[k+1] + 2) / 4,
-// with the end samples copied unless a neighbour is given.
-__global__ void upsample_422_kernel(const uint8_t *__restrict__ rows, const int16_t *__restrict__ left,
-                                    const int16_t *__restrict__ right, int32_t *__restrict__ out, int64_t n) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int s[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) s[k] = rows[i * 8 + k];
-    int32_t *o = out + i * 16;
-    int l = left[i], r = right[i];
-    o[0] = l < 0 ? s[0] : (3 * s[0] + l + 1) >> 2;
-#pragma unroll
-    for (int k = 1; k < 8; ++k) o[2 * k] = (3 * s[k] + s[k - 1] + 1) >> 2;
-#pragma unroll
-    for (int k = 0; k < 7; ++k) o[2 * k + 1] = (3 * s[k] + s[k + 1] + 2) >> 2;
-    o[15] = r < 0 ? s[7] : (3 * s[7] + r + 2) >> 2;
+    render_kernel<SUB><<<n_tiles, kThreads, bytes, stream>>>(images, tiles);
+    return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_upsample_422(const uint8_t *rows, const int16_t *left, const int16_t *right,
-                               int32_t *out, int64_t n, cudaStream_t stream) {
-    if (n <= 0) return cudaSuccess;
-    upsample_422_kernel<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(rows, left, right, out, n);
-    return cudaGetLastError();
+size_t render_smem_bytes(int sub) {
+    return sub == HJ_SUB_444 ? sizeof(Smem<HJ_SUB_444>)
+         : sub == HJ_SUB_422 ? sizeof(Smem<HJ_SUB_422>) : sizeof(Smem<HJ_SUB_420>);
 }
 
-cudaError_t launch_render(int sub, bool direct, const hj_image_t *images, const Tile *tiles,
+cudaError_t launch_render(int sub, bool /*direct is per image*/, const hj_image_t *images, const Tile *tiles,
                           int n_tiles, cudaStream_t stream) {
     if (n_tiles <= 0) return cudaSuccess;
-    dim3 grid(n_tiles), block(kThreads);
-#define HJ_LAUNCH(S, D) render_kernel<S, D><<<grid, block, 0, stream>>>(images, tiles)
-    if (sub == HJ_SUB_444) {
-        if (direct) HJ_LAUNCH(HJ_SUB_444, true); else HJ_LAUNCH(HJ_SUB_444, false);
-    } else if (sub == HJ_SUB_422) {
-        if (direct) HJ_LAUNCH(HJ_SUB_422, true); else HJ_LAUNCH(HJ_SUB_422, false);
-    } else {
-        if (direct) HJ_LAUNCH(HJ_SUB_420, true); else HJ_LAUNCH(HJ_SUB_420, false);
-    }
-#undef HJ_LAUNCH
-    return cudaGetLastError();
-}
-
-cudaError_t launch_idct_blocks(const int32_t *deq, int64_t n, uint8_t *out, double *out_f64,
-                               bool direct, cudaStream_t stream) {
-    if (n <= 0) return cudaSuccess;
-    int64_t grid = (n + 127) / 128;
-    if (direct) idct_blocks_kernel<true><<<(unsigned)grid, 128, 0, stream>>>(deq, n, out, out_f64);
-    else idct_blocks_kernel<false><<<(unsigned)grid, 128, 0, stream>>>(deq, n, out, out_f64);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_ycbcr(const uint8_t *y, const uint8_t *cb, const uint8_t *cr, uint8_t *rgb,
-                         int64_t n, cudaStream_t stream) {
-    if (n <= 0) return cudaSuccess;
-    int64_t grid = (n + 255) / 256;
-    ycbcr_kernel<<<(unsigned)grid, 256, 0, stream>>>(y, cb, cr, rgb, n);
-    return cudaGetLastError();
+    if (sub == HJ_SUB_444) return launch_sub<HJ_SUB_444>(images, tiles, n_tiles, stream);
+    if (sub == HJ_SUB_422) return launch_sub<HJ_SUB_422>(images, tiles, n_tiles, stream);
+    return launch_sub<HJ_SUB_420>(images, tiles, n_tiles, stream);
 }
 
 }  // namespace hj

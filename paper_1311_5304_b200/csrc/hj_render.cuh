@@ -20,12 +20,12 @@ struct Tile {
 };
 static_assert(sizeof(Tile) == 32, "Tile layout");
 
-// Strip widths (MCUs per CTA) chosen so one sweep step has ~128 blocks for
-// the 128 threads of the CTA: 444 -> 3*S, 422 -> 4*S+4, 420 -> 6*S+4.
+// Strip widths (MCUs per CTA) chosen so one sweep step has ~128 two-block
+// jobs for the 128 threads: 444 -> S/2 + S, 422 -> S + (S+2), 420 -> 2S + (S+2).
 constexpr int kThreads = 128;
-constexpr int kStrip444 = 42;
-constexpr int kStrip422 = 31;
-constexpr int kStrip420 = 20;
+constexpr int kStrip444 = 84;
+constexpr int kStrip422 = 63;
+constexpr int kStrip420 = 42;
 
 inline int strip_width(int sub) {
     return sub == HJ_SUB_444 ? kStrip444 : sub == HJ_SUB_422 ? kStrip422 : kStrip420;

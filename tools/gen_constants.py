@@ -115,6 +115,9 @@ def colour_constants():
     assert np.array_equal(np.broadcast_to(r_int, r_ref.shape), r_ref), "R formula"
     assert np.array_equal(np.broadcast_to(b_int, b_ref.shape), b_ref), "B formula"
     assert np.array_equal(g_int, g_ref), "G formula"
+    # the tie pair's G accumulator value must be unique over all (Cb, Cr)
+    gsum = AGB * iv[:, None] + AGR * iv[None, :] + CG
+    assert (gsum == AGB * 78 + AGR * 178 + CG).sum() == 1, "G special value not unique"
     return {"K": K, "AR": AR, "CR": CR_, "AB": AB, "CB": CB_, "AGB": AGB, "AGR": AGR,
             "CG": CG}
 
