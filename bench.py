@@ -254,12 +254,14 @@ def main():
     clocks.start()
     time.sleep(0.3)  # let the sampler attach before the timed region
     launches0 = _lib.lib.hj_launch_count()
+    exact0 = _lib.lib.hj_exact_block_count()
     e0.record(stream)
     for _ in range(args.steps):
         db.render(stream=stream)
     e1.record(stream)
     stream.synchronize()
     launches = _lib.lib.hj_launch_count() - launches0
+    exact_blocks = _lib.lib.hj_exact_block_count() - exact0
     clk = clocks.stop()
     barrier(pg)
     ms = e0.elapsed_ms(e1)
@@ -321,6 +323,8 @@ def main():
                     "steps": e2e_steps, "bit_exact_vs_oracle": exact},
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
+            "idct_screen": {"exact_fp64_block_frac": round(
+                exact_blocks / (args.steps * sum(s.n_y + 2 * s.n_c for s in db.slots)), 5)},
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

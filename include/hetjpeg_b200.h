@@ -108,6 +108,10 @@ hj_status hj_plan_destroy(void *plan);
  * (evidence for the bench's gpu_launches claim). */
 uint64_t hj_launch_count(void);
 
+/* Blocks the render kernel's binary32 screen could not prove and recomputed
+ * in exact float64 (cumulative, all launches). */
+uint64_t hj_exact_block_count(void);
+
 /* ---- the parallel phase: synchronous host-buffer drop-in -------------- */
 /* Exactly the backend contract of render_rows_444 / render_rows_422
  * (kernels/_native.pyx:532-549, kernels/fallback.py:224-260): HOST arrays,
@@ -166,6 +170,19 @@ hj_status hj_decode_mcu_rows(const uint8_t *data, int64_t n_bytes, int64_t *stat
                              int16_t *y_out, int16_t *cb_out, int16_t *cr_out,
                              int32_t row0, int32_t n_rows, int32_t mcus_per_row,
                              int32_t y_per_mcu, int32_t restart_interval);
+
+/* Throughput decoder for whole scans (pipelined / batched decode): same
+ * coefficients as hj_decode_mcu_rows, 64-bit bit buffer + 10-bit lookahead
+ * with fused run/size/value AC decode, and the scan split at its RSTn markers
+ * across up to n_threads host threads (exact: RSTn resets the predictors,
+ * kernels/_native.pyx:238-257).  Planes must be zero-initialised.
+ * hj_huff_build packs the tables once per scan header. */
+hj_status hj_huff_build(const hj_scan_tables_t *scan, void **fast);
+void hj_huff_free(void *fast);
+hj_status hj_decode_scan_fast(const void *fast, const uint8_t *data, int64_t n_bytes,
+                              int16_t *y_out, int16_t *cb_out, int16_t *cr_out,
+                              int32_t mcus_per_row, int32_t mcu_rows, int32_t y_per_mcu,
+                              int32_t restart_interval, int32_t n_threads);
 
 /* Index of the first non-restart marker after the scan data starting at
  * `start`, or -1 if the stream ends inside the entropy-coded data

@@ -15,7 +15,8 @@ import numpy as np
 
 from .errors import BadCode, BitstreamExhausted, HetJpegError, MarkerInScan
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhetjpeg_b200.so")
+_LIB_PATH = os.environ.get("HETJPEG_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libhetjpeg_b200.so")
 
 HJ_OK = 0
 HJ_ERR_EXHAUSTED = 1
@@ -94,6 +95,7 @@ _SIG = {
     "hj_plan_launch": (C.c_int, [_P, _P]),
     "hj_plan_destroy": (C.c_int, [_P]),
     "hj_launch_count": (C.c_uint64, []),
+    "hj_exact_block_count": (C.c_uint64, []),
     "hj_render_rows": (C.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
                                  _I32, _I32, _I64, _I64]),
     "hj_idct_blocks": (C.c_int, [_P, _I64, _P, _I32]),
@@ -103,6 +105,9 @@ _SIG = {
     "hj_decode_mcu_rows": (C.c_int, [_P, _I64, _P, C.POINTER(hj_scan_tables_t), _P, _P, _P, _I32,
                                      _I32, _I32, _I32, _I32]),
     "hj_scan_entropy_end": (C.c_int64, [_P, _I64, _I64]),
+    "hj_huff_build": (C.c_int, [C.POINTER(hj_scan_tables_t), C.POINTER(_P)]),
+    "hj_huff_free": (None, [_P]),
+    "hj_decode_scan_fast": (C.c_int, [_P, _P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _I32]),
 }
 for _name, (_res, _args) in _SIG.items():
     _fn = getattr(lib, _name)

@@ -330,6 +330,8 @@ hj_status hj_render_batch(const hj_image_t *images, int n_images, void *stream) 
 
 uint64_t hj_launch_count(void) { return g_launches.load(); }
 
+uint64_t hj_exact_block_count(void) { return hj::exact_block_count(); }
+
 hj_status hj_render_rows(const int16_t *y, const int16_t *cb, const int16_t *cr,
                          const int32_t *q3x64, uint8_t *rgb, int32_t width, int32_t height,
                          int32_t mcus_per_row, int32_t mcu_rows, int32_t row0, int32_t n_rows,

@@ -38,22 +38,17 @@ __constant__ float kScreenK[64] = HJ_SCREEN_K_INIT;
 
 typedef unsigned long long u64;
 
+// Blocks recomputed by the exact float64 path (all launches; diagnostics).
+__device__ unsigned long long g_exact_blocks;
+
 // ---------------------------------------------------------- packed f32x2
 __device__ __forceinline__ u64 pk(float lo, float hi) {
     u64 r;
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
     return r;
 }
-__device__ __forceinline__ float plo(u64 v) {
-    float l, h;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(l), "=f"(h) : "l"(v));
-    return l;
-}
-__device__ __forceinline__ float phi(u64 v) {
-    float l, h;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(l), "=f"(h) : "l"(v));
-    return h;
-}
+__device__ __forceinline__ float plo(u64 v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float phi(u64 v) { return __uint_as_float((uint32_t)(v >> 32)); }
 __device__ __forceinline__ u64 add2(u64 a, u64 b) {
     u64 d;
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
@@ -126,21 +121,23 @@ __device__ __forceinline__ float4 lds128f(const float *p) {
     return v;
 }
 
-// Per-sample rounding test of one f32x2 output pair.  t = v + C, C = 3200.5 -/+ Eq
-// lands in the binade [2048, 4096) (ulp 2^-12) for v in [-200, 895]: integer
-// part floor(v + 128.5) = (bits >> 12) - 0x45400.  `acc` collects
-// bits(t-) ^ bits(t+): any bit >= 12 means some bracket crosses a boundary.
-// v > 895 gives t >= 4096, n >= 1024 and a saturated 255 (correct: the true
-// sample exceeds 255.5); v < -200 is clamped (its output is 0 either way).
+// Per-sample rounding test of one f32x2 output pair (DESIGN.md "FP32
+// screen").  v is clamped below at -128.4 (every true sample below -128.4+E
+// rounds to 0 anyway), then t = v + C with C = 384.5 -/+ Eq lands in the
+// binade [256, 512) (ulp 2^-15) for v < 127.5, where floor(v + 128.5) =
+// (bits >> 15) - 0x8700.  `acc` collects bits(t-) ^ bits(t+): any bit >= 15
+// means some bracket straddles a rounding boundary (or a binade edge).
+// v >= 127.5 gives t >= 512, n >= 256 and a saturated 255 - correct, since
+// then the true sample exceeds 255.5 - E.
 __device__ __forceinline__ void round_pair(u64 v, u64 cm, u64 cp, uint32_t &acc, int &n_lo, int &n_hi) {
-    float lo = fmaxf(plo(v), -200.0f), hi = fmaxf(phi(v), -200.0f);
+    float lo = fmaxf(plo(v), -128.4f), hi = fmaxf(phi(v), -128.4f);
     u64 w = pk(lo, hi);
     u64 tm = add2(w, cm), tp = add2(w, cp);
     uint32_t a0 = __float_as_uint(plo(tm)), a1 = __float_as_uint(phi(tm));
     uint32_t b0 = __float_as_uint(plo(tp)), b1 = __float_as_uint(phi(tp));
     acc |= (a0 ^ b0) | (a1 ^ b1);
-    n_lo = (int)(a0 >> 12) - 0x45400;
-    n_hi = (int)(a1 >> 12) - 0x45400;
+    n_lo = (int)(a0 >> 15) - 0x8700;
+    n_hi = (int)(a1 >> 15) - 0x8700;
 }
 
 // FP32 screen of one block: returns true (and the 64 samples, u8 row-major,
@@ -174,12 +171,12 @@ __device__ __forceinline__ bool screen_block(const int16_t *__restrict__ src, co
             }
         }
     }
-    // bound: E = u*B*(1+2e-3) + 2^-13 (t rounding) + 2^-30 (float64 side),
-    // rounded up to the 2^-12 grid so 3200.5 +- Eq is exact in binary32
+    // bound: E = u*B*(1 + 2.5e-3) + 2^-16 (rounding of t) + 2^-30 (float64
+    // side), rounded up to the 2^-15 grid so 384.5 -/+ Eq is exact in binary32
     float B = (b0 + b1) + (b2 + b3);
-    float e = fmaf(B, 5.972e-8f, 1.2208e-4f);
-    float eq = ceilf(e * 4096.0f) * (1.0f / 4096.0f);
-    u64 cm = pk(3200.5f - eq, 3200.5f - eq), cpl = pk(3200.5f + eq, 3200.5f + eq);
+    float e = fmaf(B, 5.9754e-8f, 1.5260e-5f);
+    float eq = ceilf(e * 32768.0f) * (1.0f / 32768.0f);
+    u64 cm = pk(384.5f - eq, 384.5f - eq), cpl = pk(384.5f + eq, 384.5f + eq);
 
 #pragma unroll
     for (int cp = 0; cp < 4; ++cp)
@@ -204,40 +201,38 @@ __device__ __forceinline__ bool screen_block(const int16_t *__restrict__ src, co
         out[r1 * 2] = pack4(n1[0], n1[1], n1[2], n1[3]);
         out[r1 * 2 + 1] = pack4(n1[4], n1[5], n1[6], n1[7]);
     }
-    return (acc >> 12) == 0;
+    return (acc >> 15) == 0;
 }
 
 // ------------------------------------------------------ exact fallback
 
-// float64 IDCT of one block in the reference's exact operation order
-// (_native.pyx:364-388), column-pass results staged in shared memory
-// (`g`, 64 doubles) so the register footprint stays small.  Writes the 64
-// rounded samples (u8, row-major, 4 per word) to `out` (shared, 64 bytes).
-__device__ __noinline__ void exact_block(const int16_t *__restrict__ src, const int *q, bool direct,
-                                         double *g, uint32_t *out) {
-#pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
+// Cooperative exact float64 IDCT of one block by 8 threads (lane l = column
+// l in the column pass, row l in the row pass), the reference's operation
+// order (_native.pyx:364-388); column results staged in `g` (64 doubles,
+// shared).  Returns row l's 8 rounded samples packed in a uint2.
+__device__ __forceinline__ uint2 exact_block_x8(const int16_t *__restrict__ src, const int *q, bool direct,
+                                                double *g, int l, unsigned mask) {
+    {
         double d[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            int v = (int)src[r * 8 + c] * q[r * 8 + c];
-            d[r] = direct ? i2d(v) : dmul(i2d(v), kPre64[r * 8 + c]);
+            int v = (int)src[r * 8 + l] * q[r * 8 + l];
+            d[r] = direct ? i2d(v) : dmul(i2d(v), kPre64[r * 8 + l]);
         }
         if (direct) direct8(d, kBasis64);
         else aan8(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7]);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) g[r * 8 + c] = d[r];
+        for (int r = 0; r < 8; ++r) g[r * 8 + l] = d[r];
     }
-#pragma unroll 1
-    for (int r = 0; r < 8; ++r) {
-        double x[8];
+    __syncwarp(mask);
+    double x[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) x[k] = g[r * 8 + k];
-        if (direct) direct8(x, kBasis64);
-        else aan8(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
-        out[2 * r] = pack4(round_sample(x[0]), round_sample(x[1]), round_sample(x[2]), round_sample(x[3]));
-        out[2 * r + 1] = pack4(round_sample(x[4]), round_sample(x[5]), round_sample(x[6]), round_sample(x[7]));
-    }
+    for (int k = 0; k < 8; ++k) x[k] = g[l * 8 + k];
+    if (direct) direct8(x, kBasis64);
+    else aan8(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
+    __syncwarp(mask);
+    return make_uint2(pack4(round_sample(x[0]), round_sample(x[1]), round_sample(x[2]), round_sample(x[3])),
+                      pack4(round_sample(x[4]), round_sample(x[5]), round_sample(x[6]), round_sample(x[7])));
 }
 
 // ------------------------------------------------------------- geometry
@@ -246,31 +241,31 @@ template <int SUB>
 struct Geo;
 template <>
 struct Geo<HJ_SUB_444> {
-    static constexpr int S = kStrip444, YPM = 1, MW = 8, MH = 8;
+    static constexpr int S = kStrip444, MW = 8, MH = 8;
     static constexpr int YW = 8 * S;   // Y plane width (bytes)
     static constexpr int CW = 8 * S;   // chroma window width (words)
     static constexpr int CROWS = 8;
 };
 template <>
 struct Geo<HJ_SUB_422> {
-    static constexpr int S = kStrip422, YPM = 2, MW = 16, MH = 8;
+    static constexpr int S = kStrip422, MW = 16, MH = 8;
     static constexpr int YW = 16 * S;
     static constexpr int CW = 8 * (S + 2);
     static constexpr int CROWS = 8;
 };
 template <>
 struct Geo<HJ_SUB_420> {
-    static constexpr int S = kStrip420, YPM = 4, MW = 16, MH = 16;
+    static constexpr int S = kStrip420, MW = 16, MH = 16;
     static constexpr int YW = 16 * S;
     static constexpr int CW = 8 * (S + 2);
-    static constexpr int CROWS = 17;  // MCU rows r, r+1 (8 rows each) + last row of r-1
+    static constexpr int CROWS = 17;  // MCU rows c (slot c&1, 8 rows each) + row 16: last row of r-1
 };
 
 #ifndef HJ_MIN_CTAS
 #define HJ_MIN_CTAS 4
 #endif
-constexpr int kFallbackSlots = 8;    // concurrent exact-fallback jobs per CTA
-constexpr int kQueueMax = 256;  // >= blocks of one sweep step
+constexpr int kExactGroups = kThreads / 8;  // blocks recomputed in parallel
+constexpr int kQueueMax = 256;              // >= blocks of one sweep step
 
 template <int SUB>
 struct Smem {
@@ -279,12 +274,11 @@ struct Smem {
     uint32_t cs[G::CROWS * G::CW];          // SWAR chroma: Cb | Cr << 16
     float qf[3][64];                        // binary32 q * pre (screen)
     int qi[3][64];                          // integer q (exact path)
-    double g[kFallbackSlots][64];           // exact-path column results
-    uint32_t fout[kFallbackSlots][16];      // exact-path samples
-    uint32_t queue[kQueueMax];              // fallback jobs
+    double g[kExactGroups][64];             // exact-path column results
+    uint32_t queue[kQueueMax];              // exact-path jobs
     uint32_t qdst[kQueueMax];
     uint4 cscratch[kThreads][4];            // Cb samples of a chroma job
-    int n_queue;
+    int n_queue[2];                         // per iteration parity (reset lag)
 };
 
 __device__ __forceinline__ void write_y_rows(uint8_t *ys, int yoff, int stride, const uint32_t (&w)[16]) {
@@ -294,13 +288,15 @@ __device__ __forceinline__ void write_y_rows(uint8_t *ys, int yoff, int stride, 
 }
 
 // Interleave Cb and Cr sample rows into SWAR words: word k = cb_k | cr_k << 16.
-__device__ __forceinline__ void write_c_rows(uint32_t *cs, int coff, int stride, const uint32_t (&cb)[16],
+__device__ __forceinline__ void write_c_rows(uint32_t *cs, int coff, int stride, const uint4 *cb,
                                              const uint32_t (&cr)[16]) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
+        uint4 cbv = cb[r >> 1];
+        const uint32_t cbw[2] = {(r & 1) ? cbv.z : cbv.x, (r & 1) ? cbv.w : cbv.y};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            uint32_t a = cb[2 * r + h], b = cr[2 * r + h];
+            uint32_t a = cbw[h], b = cr[2 * r + h];
             uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
             uint4 v = make_uint4(__byte_perm(t0, 0, 0x4140), __byte_perm(t0, 0, 0x4342),
                                  __byte_perm(t1, 0, 0x4140), __byte_perm(t1, 0, 0x4342));
@@ -327,171 +323,152 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
         sm.qi[i >> 6][i & 63] = q;
         sm.qf[i >> 6][i & 63] = (float)((double)q * kPre64[i & 63]);
     }
-    if (tid == 0) sm.n_queue = 0;
+    if (tid == 0) sm.n_queue[0] = sm.n_queue[1] = 0;
 
     // chroma MCU window of the strip: [m0-1, m1+1) for 4:2:2/4:2:0
     const int cm_lo = (SUB == HJ_SUB_444) ? t.m0 : t.m0 - 1;
     const int n_cm = (SUB == HJ_SUB_444) ? S : S + 2;
     // Y jobs: two blocks each (444: MCU pair; 422: one MCU; 420: half MCU)
     const int n_yj = (SUB == HJ_SUB_444) ? (S + 1) / 2 : (SUB == HJ_SUB_422 ? S : 2 * S);
+    const bool left_edge = (t.m0 == 0), right_edge = (t.m1 == mpr);
     __syncthreads();
 
-    auto enqueue = [&](uint32_t job, uint32_t dst) {
-        int k = atomicAdd(&sm.n_queue, 1);
-        if (k < kQueueMax) {
-            sm.queue[k] = job;
-            sm.qdst[k] = dst;
-        }
-    };
-
-    // One transform job: two blocks.  Y job: blocks side by side in the Y
-    // plane; chroma job: the Cb and Cr block of one MCU into SWAR words.
-    // Queue entry: comp << 30 | block index; destination: Y byte offset, or
-    // 1 << 31 | lane << 30 | chroma word offset.
-    auto run_job = [&](int job, int row, int cslot) {
-        if (job < n_yj) {
-            // Y block k of the job: 444 MCUs 2j, 2j+1; 422 MCU j (left,
-            // right); 420 MCU j/2, blocks 0,1 (top) or 2,3 (bottom)
-            const int nb = (SUB == HJ_SUB_444 && 2 * job + 1 >= S) ? 1 : 2;
-#pragma unroll 1
-            for (int k = 0; k < nb; ++k) {
-                int64_t blk;
-                int yoff;
-                if (SUB == HJ_SUB_444) {
-                    blk = (int64_t)row * mpr + t.m0 + 2 * job + k;
-                    yoff = (2 * job + k) * 8;
-                } else if (SUB == HJ_SUB_422) {
-                    blk = ((int64_t)row * mpr + t.m0 + job) * 2 + k;
-                    yoff = job * 16 + k * 8;
-                } else {
-                    int lm = job >> 1, half = job & 1;
-                    blk = ((int64_t)row * mpr + t.m0 + lm) * 4 + 2 * half + k;
-                    yoff = half * 8 * G::YW + lm * 16 + k * 8;
-                }
-                uint32_t w[16];
-                bool ok = !direct && screen_block(im.y + blk * 64, sm.qf[0], w);
-                if (ok) write_y_rows(sm.ys, yoff, G::YW, w);
-                else enqueue((uint32_t)blk, (uint32_t)yoff);
-            }
+    // One transform job = two blocks through one screen call site.  Y job:
+    // blocks side by side in the Y plane; chroma job (job >= n_yj): the Cb
+    // and Cr block of one MCU of chroma row crow, combined into SWAR words.
+    // Exact-path queue entry: comp << 30 | block index; destination: Y byte
+    // offset, or 1 << 31 | lane << 30 | chroma word offset.
+    auto run_job = [&](int job, int yrow, int crow, int *n_queue) {
+        const bool is_y = job < n_yj;
+        int lm = is_y ? 0 : job - n_yj;
+        int64_t cblk = 0;
+        int coff = 0;
+        int nb = 2;
+        if (is_y) {
+            if (SUB == HJ_SUB_444 && 2 * job + 1 >= S) nb = 1;
         } else {
-            int lm = job - n_yj;
             int m = cm_lo + lm;
             if (m < 0 || m >= mpr) return;
-            int64_t blk = (int64_t)row * mpr + m;
-            int coff = cslot * 8 * G::CW + lm * 8;
-            bool okb, okr;
-            {
-                uint32_t wb[16];
-                okb = !direct && screen_block(im.cb + blk * 64, sm.qf[1], wb);
+            cblk = (int64_t)crow * mpr + m;
+            coff = (SUB == HJ_SUB_420 ? (crow & 1) * 8 * G::CW : 0) + lm * 8;
+            if constexpr (SUB == HJ_SUB_420) {
+                // copy-on-overwrite: the slot's old row 7 (chroma MCU row
+                // crow-2) becomes row 16, the context of MCU row crow-1
+#pragma unroll
+                for (int i = 0; i < 8; i += 4)
+                    *reinterpret_cast<uint4 *>(sm.cs + 16 * G::CW + lm * 8 + i) =
+                        *reinterpret_cast<const uint4 *>(sm.cs + coff + 7 * G::CW + i);
+            }
+        }
+        bool ok0 = false;
+#pragma unroll 1
+        for (int k = 0; k < nb; ++k) {
+            const int16_t *src;
+            const float *qf;
+            int64_t blk;
+            int yoff = 0;
+            if (is_y) {
+                if (SUB == HJ_SUB_444) {
+                    blk = (int64_t)yrow * mpr + t.m0 + 2 * job + k;
+                    yoff = (2 * job + k) * 8;
+                } else if (SUB == HJ_SUB_422) {
+                    blk = ((int64_t)yrow * mpr + t.m0 + job) * 2 + k;
+                    yoff = job * 16 + k * 8;
+                } else {
+                    int hm = job >> 1, half = job & 1;  // MCU hm, blocks 0,1 (top) / 2,3 (bottom)
+                    blk = ((int64_t)yrow * mpr + t.m0 + hm) * 4 + 2 * half + k;
+                    yoff = half * 8 * G::YW + hm * 16 + k * 8;
+                }
+                src = im.y + blk * 64;
+                qf = sm.qf[0];
+            } else {
+                blk = cblk;
+                src = (k == 0 ? im.cb : im.cr) + blk * 64;
+                qf = sm.qf[1 + k];
+            }
+            uint32_t w[16];
+            const bool ok = !direct && screen_block(src, qf, w);
+            if (is_y) {
+                if (ok) {
+                    write_y_rows(sm.ys, yoff, G::YW, w);
+                } else {
+                    int e = atomicAdd(n_queue, 1);
+                    sm.queue[e] = (uint32_t)blk;
+                    sm.qdst[e] = (uint32_t)yoff;
+                }
+            } else if (k == 0) {
+                ok0 = ok;
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    sm.cscratch[tid][i] = make_uint4(wb[4 * i], wb[4 * i + 1], wb[4 * i + 2], wb[4 * i + 3]);
-            }
-            uint32_t wr[16];
-            okr = !direct && screen_block(im.cr + blk * 64, sm.qf[2], wr);
-            if (okb && okr) {
-                uint32_t wb[16];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    uint4 v = sm.cscratch[tid][i];
-                    wb[4 * i] = v.x;
-                    wb[4 * i + 1] = v.y;
-                    wb[4 * i + 2] = v.z;
-                    wb[4 * i + 3] = v.w;
-                }
-                write_c_rows(sm.cs, coff, G::CW, wb, wr);
+                    sm.cscratch[tid][i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+            } else if (ok && ok0) {
+                write_c_rows(sm.cs, coff, G::CW, sm.cscratch[tid], w);
             } else {
-                // the exact path writes both 16-bit lanes of this MCU's words
-                enqueue((uint32_t)blk | (1u << 30), (uint32_t)coff | (1u << 31));
-                enqueue((uint32_t)blk | (2u << 30), (uint32_t)coff | (1u << 31) | (1u << 30));
+                int e = atomicAdd(n_queue, 2);
+                sm.queue[e] = (uint32_t)blk | (1u << 30);
+                sm.qdst[e] = (uint32_t)coff | (1u << 31);
+                sm.queue[e + 1] = (uint32_t)blk | (2u << 30);
+                sm.qdst[e + 1] = (uint32_t)coff | (1u << 31) | (1u << 30);
             }
         }
     };
 
-    auto fallback_pass = [&]() {
+    // 4:2:0 sweeps one iteration ahead on chroma: iteration `it` transforms
+    // the Y blocks of MCU row it and the chroma of MCU row it+1, starting two
+    // iterations early (transform-only) to bring in rows r0-1 and r0.
+    const int it0 = (SUB == HJ_SUB_420) ? max(t.r0 - 2, -1) : t.r0;
+#pragma unroll 1
+    for (int it = it0; it < t.r1; ++it) {
+        const bool draw = it >= t.r0;
+        int crow = it, n_c = n_cm;
+        if (SUB == HJ_SUB_420) {
+            crow = it + 1;
+            n_c = (crow >= t.r0 - 1 && crow >= 0 && crow < im.mcu_rows) ? n_cm : 0;
+        }
+        const int n_y = draw ? n_yj : 0;
+        // ---- (1) binary32 screen of this iteration's blocks
+#pragma unroll 1
+        int *const nq = &sm.n_queue[it & 1];
+        for (int j = tid; j < n_y + n_c; j += kThreads) run_job(j < n_y ? j : n_yj + (j - n_y), it, crow, nq);
         __syncthreads();
-        const int n = min(sm.n_queue, kQueueMax);
-        if (tid < kFallbackSlots) {
-            for (int e = tid; e < n; e += kFallbackSlots) {
-                uint32_t job = sm.queue[e], dst = sm.qdst[e];
-                int comp = job >> 30;
-                int64_t blk = job & 0x3fffffff;
+        // ---- (2) exact float64 recompute of the unproven blocks, 8 threads each
+        {
+            const int n = *nq;
+            const int grp = tid >> 3, l = tid & 7;
+            const unsigned gmask = 0xffu << (tid & 24);  // the 8 lanes of this group
+#pragma unroll 1
+            for (int e = grp; e < n; e += kExactGroups) {
+                const uint32_t job = sm.queue[e], dst = sm.qdst[e];
+                const int comp = job >> 30;
+                const int64_t blk = job & 0x3fffffff;
                 const int16_t *src = (comp == 0 ? im.y : comp == 1 ? im.cb : im.cr) + blk * 64;
-                exact_block(src, sm.qi[comp], direct, sm.g[tid], sm.fout[tid]);
-                const uint32_t *o = sm.fout[tid];
+                const uint2 row = exact_block_x8(src, sm.qi[comp], direct, sm.g[grp], l, gmask);
                 if (!(dst >> 31)) {
-                    for (int r = 0; r < 8; ++r)
-                        *reinterpret_cast<uint2 *>(sm.ys + dst + r * G::YW) = make_uint2(o[2 * r], o[2 * r + 1]);
+                    *reinterpret_cast<uint2 *>(sm.ys + dst + l * G::YW) = row;
                 } else {
-                    int coff = dst & 0x3fffffff, lane = (dst >> 30) & 1;
-                    uint16_t *cs16 = reinterpret_cast<uint16_t *>(sm.cs);
-                    const uint8_t *ob = reinterpret_cast<const uint8_t *>(o);
-                    for (int r = 0; r < 8; ++r)
-                        for (int c = 0; c < 8; ++c) cs16[2 * (coff + r * G::CW + c) + lane] = ob[r * 8 + c];
+                    const int coff = dst & 0x3fffffff, lane = (dst >> 30) & 1;
+                    uint16_t *c16 = reinterpret_cast<uint16_t *>(sm.cs + coff + l * G::CW) + lane;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) c16[2 * c] = (uint16_t)((c < 4 ? row.x >> (8 * c) : row.y >> (8 * (c - 4))) & 0xff);
                 }
             }
+            if (tid == 0 && n) atomicAdd(&g_exact_blocks, (unsigned long long)n);
         }
         __syncthreads();
-        if (tid == 0) sm.n_queue = 0;
-    };
+        // this parity's counter is next used two iterations (>= 2 barriers) later
+        if (tid == 0) *nq = 0;
+        if (!draw) continue;
 
-    // edge replication of the padded chroma plane at the image's left/right
-    // edge (fallback.py:200-212 / _native.pyx:477-480 edge copy)
-    auto edge_fix = [&](int cslot) {
-        if (SUB == HJ_SUB_444) return;
-        for (int r = tid; r < 16; r += kThreads) {
-            uint32_t *row = sm.cs + (cslot * 8 + (r & 7)) * G::CW;
-            if (r < 8 && t.m0 == 0) row[7] = row[8];
-            if (r >= 8 && t.m1 == mpr) row[8 * (S + 1)] = row[8 * (S + 1) - 1];
-        }
-    };
-
-    // 4:2:0 chroma rows: MCU row rr lives in slot rr & 1 (rows 0-7 / 8-15);
-    // row 16 keeps sample row 7 of MCU row r-1 (the filter's upper context).
-    auto save_prev_last = [&](int rr) {
-        const uint32_t *src = sm.cs + ((rr & 1) * 8 + 7) * G::CW;
-        for (int i = tid; i < G::CW; i += kThreads) sm.cs[16 * G::CW + i] = src[i];
-    };
-    if (SUB == HJ_SUB_420) {
-        if (t.r0 > 0) {  // transform MCU row r0-1 and keep its last sample row
-            for (int j = tid; j < n_cm; j += kThreads) run_job(n_yj + j, t.r0 - 1, (t.r0 - 1) & 1);
-            fallback_pass();
-            edge_fix((t.r0 - 1) & 1);
-            __syncthreads();
-            save_prev_last(t.r0 - 1);
-            __syncthreads();
-        }
-        for (int j = tid; j < n_cm; j += kThreads) run_job(n_yj + j, t.r0, t.r0 & 1);
-        fallback_pass();
-        edge_fix(t.r0 & 1);
-    }
-
-#pragma unroll 1
-    for (int row = t.r0; row < t.r1; ++row) {
-        // ---- (1) screen transforms of this step
-        int c_row = row, n_c = n_cm;
-        if (SUB == HJ_SUB_420) {
-            c_row = row + 1;
-            n_c = (c_row < im.mcu_rows) ? n_cm : 0;
-        }
-        const int cslot = (SUB == HJ_SUB_420) ? (c_row & 1) : 0;
-#pragma unroll 1
-        for (int j = tid; j < n_yj + n_c; j += kThreads) run_job(j, row, cslot);
-        // ---- (2) exact fallback
-        fallback_pass();
-        if (n_c) edge_fix(cslot);
-        __syncthreads();
-
-        // ---- (3) upsample + colour + store
-        const int y_base = row * G::MH;
+        // ---- (3) upsample + colour + store MCU row `it`
+        const int y_base = it * G::MH;
         const int n_groups = (G::MW / 8) * S;
         const int x_base = t.m0 * G::MW;
 #pragma unroll 1
-        for (int it = tid; it < G::MH * n_groups; it += kThreads) {
-            int oy = it / n_groups, gx = it - oy * n_groups;
-            int y = y_base + oy;
-            int x0 = x_base + gx * 8;
-            int npx = min(8, im.width - x0);
+        for (int item = tid; item < G::MH * n_groups; item += kThreads) {
+            const int oy = item / n_groups, gx = item - oy * n_groups;
+            const int y = y_base + oy;
+            const int x0 = x_base + gx * 8;
+            const int npx = min(8, im.width - x0);
             if (y >= im.height || npx <= 0) continue;
             uint2 yv = *reinterpret_cast<const uint2 *>(sm.ys + oy * G::YW + gx * 8);
             int Y[8];
@@ -511,18 +488,22 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     crv[i] = w[i] >> 16;
                 }
             } else {
-                // window-local chroma column of sample k0 = 8*m0 + 4*gx
+                // chroma samples k0-1 .. k0+4 (k0 = 8*m0 + 4*gx) as window-local
+                // words; the padded plane's first/last column is replicated
+                // (fallback.py:200-212, _native.pyx:477-480)
                 const int kl = 8 * (t.m0 - cm_lo) + 4 * gx;
+                const int dl = (left_edge && gx == 0) ? 0 : -1;
+                const int dr = (right_edge && gx == n_groups - 1) ? 3 : 4;
                 uint32_t c[6];
                 if (SUB == HJ_SUB_422) {
                     const uint32_t *cr = sm.cs + oy * G::CW + kl;
                     uint4 mid = *reinterpret_cast<const uint4 *>(cr);
-                    c[0] = cr[-1];
+                    c[0] = cr[dl];
                     c[1] = mid.x;
                     c[2] = mid.y;
                     c[3] = mid.z;
                     c[4] = mid.w;
-                    c[5] = cr[4];
+                    c[5] = cr[dr];
                     // h2v1: even (3c+prev+1)>>2, odd (3c+next+2)>>2 per 16-bit lane
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
@@ -534,23 +515,25 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                         crv[2 * i + 1] = od >> 18;
                     }
                 } else {
+                    // near chroma row ci, far row cf (clamped to the padded plane)
                     const int ch_img = 8 * im.mcu_rows;
-                    int ci = 8 * row + (oy >> 1);
-                    int cf = min(max(ci + ((oy & 1) ? 1 : -1), 0), ch_img - 1);
-                    // sample row -> smem row: MCU row r in slot r&1, r+1 in the other,
-                    // row 8r-1 in the saved row 16
-                    const int rn = (row & 1) * 8 + (ci & 7);
-                    const int rf = cf < 8 * row ? 16 : (((cf >> 3) & 1) * 8 + (cf & 7));
+                    const int ci = 8 * it + (oy >> 1);
+                    const int cf = min(max(ci + ((oy & 1) ? 1 : -1), 0), ch_img - 1);
+                    // row 8*it-1: saved in row 16 when this iteration overwrote
+                    // its slot with MCU row it+1, else still in slot (it-1)&1
+                    const int rn = (it & 1) * 8 + (ci & 7);
+                    const int rf = cf >= 8 * it ? (((cf >> 3) & 1) * 8 + (cf & 7))
+                                 : (it + 1 < im.mcu_rows ? 16 : ((it - 1) & 1) * 8 + 7);
                     const uint32_t *cn = sm.cs + rn * G::CW + kl;
                     const uint32_t *cfp = sm.cs + rf * G::CW + kl;
                     uint4 mn = *reinterpret_cast<const uint4 *>(cn), mf = *reinterpret_cast<const uint4 *>(cfp);
                     // colsum = 3*near + far per lane (libjpeg h2v2 fancy)
-                    c[0] = cn[-1] * 3u + cfp[-1];
+                    c[0] = cn[dl] * 3u + cfp[dl];
                     c[1] = mn.x * 3u + mf.x;
                     c[2] = mn.y * 3u + mf.y;
                     c[3] = mn.z * 3u + mf.z;
                     c[4] = mn.w * 3u + mf.w;
-                    c[5] = cn[4] * 3u + cfp[4];
+                    c[5] = cn[dr] * 3u + cfp[dr];
                     // even (3cs+prev+8)>>4, odd (3cs+next+7)>>4
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
@@ -576,10 +559,6 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
             store_rgb8(im.rgb + ((int64_t)y * im.width + x0) * 3, w, npx);
         }
         __syncthreads();
-        if (SUB == HJ_SUB_420 && row + 1 < t.r1) {
-            save_prev_last(row);
-            __syncthreads();
-        }
     }
 }
 
@@ -598,6 +577,12 @@ cudaError_t launch_sub(const hj_image_t *images, const Tile *tiles, int n_tiles,
 }
 
 }  // namespace
+
+unsigned long long exact_block_count() {
+    unsigned long long v = 0;
+    cudaMemcpyFromSymbol(&v, g_exact_blocks, sizeof(v));
+    return v;
+}
 
 size_t render_smem_bytes(int sub) {
     return sub == HJ_SUB_444 ? sizeof(Smem<HJ_SUB_444>)

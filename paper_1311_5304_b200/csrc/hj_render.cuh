@@ -36,6 +36,9 @@ inline int strip_width(int sub) {
 cudaError_t launch_render(int subsampling, bool direct, const hj_image_t *images,
                           const Tile *tiles, int n_tiles, cudaStream_t stream);
 
+// Blocks the FP32 screen sent to the exact float64 path, all launches so far.
+unsigned long long exact_block_count();
+
 // Single-block transforms (reference per-block API).
 cudaError_t launch_idct_blocks(const int32_t *deq, int64_t n, uint8_t *out, double *out_f64,
                                bool direct, cudaStream_t stream);

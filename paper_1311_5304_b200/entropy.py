@@ -163,6 +163,46 @@ def decode_rows(cursor: EntropyCursor, parsed: ParsedJpeg, out: CoefficientBuffe
     return cursor
 
 
+class FastScan:
+    """Whole-scan throughput decoder (hj_decode_scan_fast) for one parsed
+    header; bit-identical coefficients to `decode_all`."""
+
+    def __init__(self, parsed: ParsedJpeg):
+        self.parsed = parsed
+        self.geometry = geometry_of(parsed)
+        tables = _lib.hj_scan_tables_t()
+        from .kernels import cuda as _backend
+        tables = _backend.prepare_scan(*_pack_scan_tables(parsed))
+        h = _lib.C.c_void_p()
+        _lib.check(_lib.lib.hj_huff_build(_lib.C.byref(tables), _lib.C.byref(h)), "hj_huff_build")
+        self._h = h.value
+
+    def decode(self, data: bytes | None = None, out: CoefficientBuffer | None = None,
+               threads: int = 1, pinned: bool = False) -> CoefficientBuffer:
+        p = self.parsed
+        data = p.stream if data is None else data
+        sp = p.entropy_span
+        buf = np.frombuffer(data, dtype=np.uint8)[sp.offset:sp.offset + sp.length]
+        if out is None:
+            out = alloc_coefficients(self.geometry, pinned=pinned)
+        else:
+            out.y_blocks[...] = 0
+            out.cb_blocks[...] = 0
+            out.cr_blocks[...] = 0
+        g = self.geometry
+        st = _lib.lib.hj_decode_scan_fast(self._h, buf.ctypes.data, len(buf), out.y_blocks.ctypes.data,
+                                          out.cb_blocks.ctypes.data, out.cr_blocks.ctypes.data,
+                                          g.mcus_per_row, g.mcu_rows, g.y_blocks_per_mcu,
+                                          p.restart_interval, int(threads))
+        _lib.check(st, "decode_scan_fast")
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.lib.hj_huff_free(self._h)
+            self._h = None
+
+
 def decode_all(parsed: ParsedJpeg, data: bytes | None = None, pinned: bool = False):
     cursor = new_cursor(parsed, data)
     buf = alloc_coefficients(cursor.geometry, pinned=pinned)

@@ -155,3 +155,22 @@ def test_entropy_end_scan_matches_python_walk():
                 continue
             break
         assert parser.scan_entropy_end(g.jpeg, start) == pos
+
+
+@pytest.mark.parametrize("g", GOLDEN_CASES, ids=repr)
+@pytest.mark.parametrize("threads", [1, 4])
+def test_fast_scan_decoder_matches_reference(g, threads):
+    p = parser.parse_stream(g.jpeg)
+    out = entropy.FastScan(p).decode(g.jpeg, threads=threads)
+    assert np.array_equal(out.y_blocks, g.y)
+    assert np.array_equal(out.cb_blocks, g.cb)
+    assert np.array_equal(out.cr_blocks, g.cr)
+
+
+def test_fast_scan_decoder_truncated_raises():
+    g = GOLDEN_CASES[-1]
+    p = parser.parse_stream(g.jpeg)
+    sp = p.entropy_span
+    cut = g.jpeg[:sp.offset + sp.length // 2] + b"\xff\xd9"
+    with pytest.raises(errors.BitstreamExhausted):
+        entropy.FastScan(p).decode(cut)
