@@ -56,7 +56,7 @@ hj_status validate(const hj_image_t &im) {
 }
 
 // Tile planning: strips of ~kStrip MCU columns, row segments of T rows, with
-// T chosen so the whole batch gives ~6 waves of CTAs (3 resident per SM).
+// T chosen so the whole batch gives ~6 waves of resident CTAs.
 struct Plan {
     // device buffer: [hj_image_t x n_images][Tile x n_tiles]
     void *dev = nullptr;
@@ -72,7 +72,7 @@ void build_tiles(const hj_image_t *images, int n, std::vector<hj::Tile> &tiles,
     int sms = 148;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t target = (int64_t)sms * 3 * 6;
+    const int64_t target = (int64_t)sms * hj::kCtasPerSm * 6;  // ~6 waves of resident CTAs
     for (int sub = HJ_SUB_444; sub <= HJ_SUB_420; ++sub) {
         for (int direct = 0; direct < 2; ++direct) {
             int64_t strip_rows = 0;

@@ -239,33 +239,33 @@ __device__ __forceinline__ uint2 exact_block_x8(const int16_t *__restrict__ src,
 
 template <int SUB>
 struct Geo;
+// Chroma SWAR words hold (c << CSH) | (c << CSH) << 16: 4:2:0 scales by 16 and
+// 4:2:2 by 64 so the fancy filters' results land byte-aligned (the filtered
+// value is byte 1 / byte 3 of the word; every lane stays below 2^16).
 template <>
 struct Geo<HJ_SUB_444> {
-    static constexpr int S = kStrip444, MW = 8, MH = 8;
+    static constexpr int S = kStrip444, MW = 8, MH = 8, CSH = 0;
     static constexpr int YW = 8 * S;   // Y plane width (bytes)
     static constexpr int CW = 8 * S;   // chroma window width (words)
     static constexpr int CROWS = 8;
 };
 template <>
 struct Geo<HJ_SUB_422> {
-    static constexpr int S = kStrip422, MW = 16, MH = 8;
+    static constexpr int S = kStrip422, MW = 16, MH = 8, CSH = 6;
     static constexpr int YW = 16 * S;
     static constexpr int CW = 8 * (S + 2);
     static constexpr int CROWS = 8;
 };
 template <>
 struct Geo<HJ_SUB_420> {
-    static constexpr int S = kStrip420, MW = 16, MH = 16;
+    static constexpr int S = kStrip420, MW = 16, MH = 16, CSH = 4;
     static constexpr int YW = 16 * S;
     static constexpr int CW = 8 * (S + 2);
     static constexpr int CROWS = 17;  // MCU rows c (slot c&1, 8 rows each) + row 16: last row of r-1
 };
 
-#ifndef HJ_MIN_CTAS
-#define HJ_MIN_CTAS 4
-#endif
 constexpr int kExactGroups = kThreads / 8;  // blocks recomputed in parallel
-constexpr int kQueueMax = 256;              // >= blocks of one sweep step
+constexpr int kQueueMax = 2 * kThreads;     // >= blocks of one sweep step
 
 template <int SUB>
 struct Smem {
@@ -287,7 +287,9 @@ __device__ __forceinline__ void write_y_rows(uint8_t *ys, int yoff, int stride, 
         *reinterpret_cast<uint2 *>(ys + yoff + r * stride) = make_uint2(w[2 * r], w[2 * r + 1]);
 }
 
-// Interleave Cb and Cr sample rows into SWAR words: word k = cb_k | cr_k << 16.
+// Interleave Cb and Cr sample rows into SWAR words:
+// word k = (cb_k | cr_k << 16) << CSH.
+template <int CSH>
 __device__ __forceinline__ void write_c_rows(uint32_t *cs, int coff, int stride, const uint4 *cb,
                                              const uint32_t (&cr)[16]) {
 #pragma unroll
@@ -298,8 +300,8 @@ __device__ __forceinline__ void write_c_rows(uint32_t *cs, int coff, int stride,
         for (int h = 0; h < 2; ++h) {
             uint32_t a = cbw[h], b = cr[2 * r + h];
             uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
-            uint4 v = make_uint4(__byte_perm(t0, 0, 0x4140), __byte_perm(t0, 0, 0x4342),
-                                 __byte_perm(t1, 0, 0x4140), __byte_perm(t1, 0, 0x4342));
+            uint4 v = make_uint4(__byte_perm(t0, 0, 0x4140) << CSH, __byte_perm(t0, 0, 0x4342) << CSH,
+                                 __byte_perm(t1, 0, 0x4140) << CSH, __byte_perm(t1, 0, 0x4342) << CSH);
             *reinterpret_cast<uint4 *>(cs + coff + r * stride + 4 * h) = v;
         }
     }
@@ -331,64 +333,74 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
     // Y jobs: two blocks each (444: MCU pair; 422: one MCU; 420: half MCU)
     const int n_yj = (SUB == HJ_SUB_444) ? (S + 1) / 2 : (SUB == HJ_SUB_422 ? S : 2 * S);
     const bool left_edge = (t.m0 == 0), right_edge = (t.m1 == mpr);
+    const int n_groups = (G::MW / 8) * S;  // 8-pixel groups per pixel row of the strip
+    const int oy0 = tid / n_groups, gx0 = tid - oy0 * n_groups;
+    const int ystep = kThreads / n_groups, gstep = kThreads - ystep * n_groups;
     __syncthreads();
 
-    // One transform job = two blocks through one screen call site.  Y job:
-    // blocks side by side in the Y plane; chroma job (job >= n_yj): the Cb
-    // and Cr block of one MCU of chroma row crow, combined into SWAR words.
+    // One transform job = two blocks through one screen call site, kept
+    // branch-free up to the call so a warp mixing Y and chroma jobs runs the
+    // screen once per block slot (no divergent duplication).  Y job: blocks
+    // side by side in the Y plane; chroma job (job >= n_yj): the Cb and Cr
+    // block of one MCU of chroma row crow, combined into SWAR words.
     // Exact-path queue entry: comp << 30 | block index; destination: Y byte
     // offset, or 1 << 31 | lane << 30 | chroma word offset.
-    auto run_job = [&](int job, int yrow, int crow, int *n_queue) {
+    auto run_job = [&](int job, int yrow, int crow, int *n_queue, bool active) {
         const bool is_y = job < n_yj;
-        int lm = is_y ? 0 : job - n_yj;
-        int64_t cblk = 0;
-        int coff = 0;
-        int nb = 2;
-        if (is_y) {
-            if (SUB == HJ_SUB_444 && 2 * job + 1 >= S) nb = 1;
-        } else {
-            int m = cm_lo + lm;
-            if (m < 0 || m >= mpr) return;
-            cblk = (int64_t)crow * mpr + m;
-            coff = (SUB == HJ_SUB_420 ? (crow & 1) * 8 * G::CW : 0) + lm * 8;
-            if constexpr (SUB == HJ_SUB_420) {
-                // copy-on-overwrite: the slot's old row 7 (chroma MCU row
-                // crow-2) becomes row 16, the context of MCU row crow-1
+        const int lm = job - n_yj;                 // chroma window MCU
+        const int m = cm_lo + lm;
+        const bool valid = active && (is_y || (m >= 0 && m < mpr));
+        const int nb = (SUB == HJ_SUB_444 && is_y && 2 * job + 1 >= S) ? 1 : 2;
+        // Y: first block index and plane offset of the job
+        int64_t yblk;
+        int yoff0;
+        if (SUB == HJ_SUB_444) {
+            yblk = (int64_t)yrow * mpr + t.m0 + 2 * job;
+            yoff0 = 2 * job * 8;
+        } else if (SUB == HJ_SUB_422) {
+            yblk = ((int64_t)yrow * mpr + t.m0 + job) * 2;
+            yoff0 = job * 16;
+        } else {  // MCU job/2, blocks 0,1 (top) or 2,3 (bottom)
+            yblk = ((int64_t)yrow * mpr + t.m0 + (job >> 1)) * 4 + 2 * (job & 1);
+            yoff0 = (job & 1) * 8 * G::YW + (job >> 1) * 16;
+        }
+        const int64_t cblk = (int64_t)crow * mpr + m;
+        const int coff = (SUB == HJ_SUB_420 ? (crow & 1) * 8 * G::CW : 0) + lm * 8;
+        if constexpr (SUB == HJ_SUB_420) {
+            // copy-on-overwrite: the slot's old row 7 (chroma MCU row crow-2)
+            // becomes row 16, the context of MCU row crow-1
+            if (valid && !is_y) {
 #pragma unroll
                 for (int i = 0; i < 8; i += 4)
                     *reinterpret_cast<uint4 *>(sm.cs + 16 * G::CW + lm * 8 + i) =
                         *reinterpret_cast<const uint4 *>(sm.cs + coff + 7 * G::CW + i);
             }
         }
+        // the same job of the next iteration reads the blocks one MCU row
+        // down: pull them into L2 now (hides DRAM latency next iteration)
+        if (valid) {
+            const bool more = is_y ? (yrow + 1 < t.r1) : (crow + 1 < im.mcu_rows && crow + 1 <= t.r1);
+            if (more) {
+                const int64_t ystep = (int64_t)mpr * (G::MW / 8) * (G::MH / 8);  // Y blocks per MCU row
+                const int16_t *p0 = is_y ? im.y + (yblk + ystep) * 64 : im.cb + (cblk + mpr) * 64;
+                const int16_t *p1 = is_y ? p0 + 64 : im.cr + (cblk + mpr) * 64;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p0));
+                if (nb > 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(p1));
+            }
+        }
         bool ok0 = false;
 #pragma unroll 1
-        for (int k = 0; k < nb; ++k) {
-            const int16_t *src;
-            const float *qf;
-            int64_t blk;
-            int yoff = 0;
-            if (is_y) {
-                if (SUB == HJ_SUB_444) {
-                    blk = (int64_t)yrow * mpr + t.m0 + 2 * job + k;
-                    yoff = (2 * job + k) * 8;
-                } else if (SUB == HJ_SUB_422) {
-                    blk = ((int64_t)yrow * mpr + t.m0 + job) * 2 + k;
-                    yoff = job * 16 + k * 8;
-                } else {
-                    int hm = job >> 1, half = job & 1;  // MCU hm, blocks 0,1 (top) / 2,3 (bottom)
-                    blk = ((int64_t)yrow * mpr + t.m0 + hm) * 4 + 2 * half + k;
-                    yoff = half * 8 * G::YW + hm * 16 + k * 8;
-                }
-                src = im.y + blk * 64;
-                qf = sm.qf[0];
-            } else {
-                blk = cblk;
-                src = (k == 0 ? im.cb : im.cr) + blk * 64;
-                qf = sm.qf[1 + k];
-            }
+        for (int k = 0; k < 2; ++k) {
+            const bool run = valid && k < nb;
+            const int64_t blk = is_y ? yblk + k : cblk;
+            const int16_t *src = (is_y ? im.y : (k == 0 ? im.cb : im.cr)) + blk * 64;
+            const float *qf = sm.qf[is_y ? 0 : 1 + k];
             uint32_t w[16];
-            const bool ok = !direct && screen_block(src, qf, w);
+            bool ok = false;
+            if (run) ok = !direct && screen_block(src, qf, w);
+            if (!run) continue;
             if (is_y) {
+                const int yoff = yoff0 + k * 8;
                 if (ok) {
                     write_y_rows(sm.ys, yoff, G::YW, w);
                 } else {
@@ -402,7 +414,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                 for (int i = 0; i < 4; ++i)
                     sm.cscratch[tid][i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
             } else if (ok && ok0) {
-                write_c_rows(sm.cs, coff, G::CW, sm.cscratch[tid], w);
+                write_c_rows<G::CSH>(sm.cs, coff, G::CW, sm.cscratch[tid], w);
             } else {
                 int e = atomicAdd(n_queue, 2);
                 sm.queue[e] = (uint32_t)blk | (1u << 30);
@@ -427,9 +439,15 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
         }
         const int n_y = draw ? n_yj : 0;
         // ---- (1) binary32 screen of this iteration's blocks
-#pragma unroll 1
         int *const nq = &sm.n_queue[it & 1];
-        for (int j = tid; j < n_y + n_c; j += kThreads) run_job(j < n_y ? j : n_yj + (j - n_y), it, crow, nq);
+        // every lane runs the job loop the same number of times (inactive
+        // lanes ride along) so the screen is never split by divergence
+        const int n_jobs = n_y + n_c;
+#pragma unroll 1
+        for (int j0 = 0; j0 < n_jobs; j0 += kThreads) {
+            const int j = j0 + tid;
+            run_job(j < n_y ? j : n_yj + (j - n_y), it, crow, nq, j < n_jobs);
+        }
         __syncthreads();
         // ---- (2) exact float64 recompute of the unproven blocks, 8 threads each
         {
@@ -449,7 +467,8 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     const int coff = dst & 0x3fffffff, lane = (dst >> 30) & 1;
                     uint16_t *c16 = reinterpret_cast<uint16_t *>(sm.cs + coff + l * G::CW) + lane;
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) c16[2 * c] = (uint16_t)((c < 4 ? row.x >> (8 * c) : row.y >> (8 * (c - 4))) & 0xff);
+                    for (int c = 0; c < 8; ++c)
+                        c16[2 * c] = (uint16_t)(((c < 4 ? row.x >> (8 * c) : row.y >> (8 * (c - 4))) & 0xff) << G::CSH);
                 }
             }
             if (tid == 0 && n) atomicAdd(&g_exact_blocks, (unsigned long long)n);
@@ -461,31 +480,35 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
 
         // ---- (3) upsample + colour + store MCU row `it`
         const int y_base = it * G::MH;
-        const int n_groups = (G::MW / 8) * S;
         const int x_base = t.m0 * G::MW;
+        const int ylim = min(G::MH, im.height - y_base);
+        // items (oy, gx) = 8 pixels, walked without a division per item
+        int oy = oy0, gx = gx0;
 #pragma unroll 1
-        for (int item = tid; item < G::MH * n_groups; item += kThreads) {
-            const int oy = item / n_groups, gx = item - oy * n_groups;
-            const int y = y_base + oy;
+        for (; oy < ylim; gx += gstep, oy += ystep) {
+            if (gx >= n_groups) {
+                gx -= n_groups;
+                ++oy;
+                if (oy >= ylim) break;
+            }
             const int x0 = x_base + gx * 8;
             const int npx = min(8, im.width - x0);
-            if (y >= im.height || npx <= 0) continue;
-            uint2 yv = *reinterpret_cast<const uint2 *>(sm.ys + oy * G::YW + gx * 8);
-            int Y[8];
+            if (npx <= 0) continue;
+            const uint2 yv = *reinterpret_cast<const uint2 *>(sm.ys + oy * G::YW + gx * 8);
+            int Y[8], cbv[8], crv[8];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                Y[i] = (yv.x >> (8 * i)) & 0xff;
-                Y[4 + i] = (yv.y >> (8 * i)) & 0xff;
+                Y[i] = (int)__byte_perm(yv.x, 0, 0x4440 + i);
+                Y[4 + i] = (int)__byte_perm(yv.y, 0, 0x4440 + i);
             }
-            int cbv[8], crv[8];
             if (SUB == HJ_SUB_444) {
                 const uint32_t *cr = sm.cs + oy * G::CW + gx * 8;
                 uint4 a = *reinterpret_cast<const uint4 *>(cr), b = *reinterpret_cast<const uint4 *>(cr + 4);
                 const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    cbv[i] = w[i] & 0xff;
-                    crv[i] = w[i] >> 16;
+                    cbv[i] = (int)__byte_perm(w[i], 0, 0x4440);
+                    crv[i] = (int)__byte_perm(w[i], 0, 0x4442);
                 }
             } else {
                 // chroma samples k0-1 .. k0+4 (k0 = 8*m0 + 4*gx) as window-local
@@ -495,6 +518,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                 const int dl = (left_edge && gx == 0) ? 0 : -1;
                 const int dr = (right_edge && gx == n_groups - 1) ? 3 : 4;
                 uint32_t c[6];
+                uint32_t rnd_e, rnd_o;
                 if (SUB == HJ_SUB_422) {
                     const uint32_t *cr = sm.cs + oy * G::CW + kl;
                     uint4 mid = *reinterpret_cast<const uint4 *>(cr);
@@ -504,16 +528,9 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     c[3] = mid.z;
                     c[4] = mid.w;
                     c[5] = cr[dr];
-                    // h2v1: even (3c+prev+1)>>2, odd (3c+next+2)>>2 per 16-bit lane
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        uint32_t t3 = c[i + 1] * 3u + 0x00010001u;
-                        uint32_t ev = t3 + c[i], od = t3 + c[i + 2] + 0x00010001u;
-                        cbv[2 * i] = (ev >> 2) & 0xff;
-                        crv[2 * i] = ev >> 18;
-                        cbv[2 * i + 1] = (od >> 2) & 0xff;
-                        crv[2 * i + 1] = od >> 18;
-                    }
+                    // h2v1 on 64x-scaled lanes: even 64(3c+prev+1), odd 64(3c+next+2)
+                    rnd_e = 0x00400040u;
+                    rnd_o = 0x00800080u;
                 } else {
                     // near chroma row ci, far row cf (clamped to the padded plane)
                     const int ch_img = 8 * im.mcu_rows;
@@ -527,23 +544,26 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     const uint32_t *cn = sm.cs + rn * G::CW + kl;
                     const uint32_t *cfp = sm.cs + rf * G::CW + kl;
                     uint4 mn = *reinterpret_cast<const uint4 *>(cn), mf = *reinterpret_cast<const uint4 *>(cfp);
-                    // colsum = 3*near + far per lane (libjpeg h2v2 fancy)
+                    // colsum = 3*near + far per lane (libjpeg h2v2 fancy), 16x scaled
                     c[0] = cn[dl] * 3u + cfp[dl];
                     c[1] = mn.x * 3u + mf.x;
                     c[2] = mn.y * 3u + mf.y;
                     c[3] = mn.z * 3u + mf.z;
                     c[4] = mn.w * 3u + mf.w;
                     c[5] = cn[dr] * 3u + cfp[dr];
-                    // even (3cs+prev+8)>>4, odd (3cs+next+7)>>4
+                    // even 16(3cs+prev+8), odd 16(3cs+next+7)
+                    rnd_e = 0x00800080u;
+                    rnd_o = 0x00700070u;
+                }
+                // filtered value = byte 1 (Cb) / byte 3 (Cr) of each word
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        uint32_t t3 = c[i + 1] * 3u + 0x00080008u;
-                        uint32_t ev = t3 + c[i], od = t3 + c[i + 2] - 0x00010001u;
-                        cbv[2 * i] = (ev >> 4) & 0xff;
-                        crv[2 * i] = ev >> 20;
-                        cbv[2 * i + 1] = (od >> 4) & 0xff;
-                        crv[2 * i + 1] = od >> 20;
-                    }
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t t3 = c[i + 1] * 3u;
+                    const uint32_t ev = t3 + c[i] + rnd_e, od = t3 + c[i + 2] + rnd_o;
+                    cbv[2 * i] = (int)__byte_perm(ev, 0, 0x4441);
+                    crv[2 * i] = (int)(ev >> 24);
+                    cbv[2 * i + 1] = (int)__byte_perm(od, 0, 0x4441);
+                    crv[2 * i + 1] = (int)(od >> 24);
                 }
             }
             Rgb p[8];
@@ -556,7 +576,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
             }
             uint32_t w[6];
             pack_rgb8(p, w);
-            store_rgb8(im.rgb + ((int64_t)y * im.width + x0) * 3, w, npx);
+            store_rgb8(im.rgb + ((int64_t)(y_base + oy) * im.width + x0) * 3, w, npx);
         }
         __syncthreads();
     }

@@ -20,12 +20,21 @@ struct Tile {
 };
 static_assert(sizeof(Tile) == 32, "Tile layout");
 
-// Strip widths (MCUs per CTA) chosen so one sweep step has ~128 two-block
-// jobs for the 128 threads: 444 -> S/2 + S, 422 -> S + (S+2), 420 -> 2S + (S+2).
-constexpr int kThreads = 128;
-constexpr int kStrip444 = 84;
-constexpr int kStrip422 = 63;
-constexpr int kStrip420 = 42;
+// CTA size and residency (one CTA = one warp by default: warps sweep their
+// strips independently, synchronising only with warp barriers).
+#ifndef HJ_THREADS
+#define HJ_THREADS 32
+#endif
+#ifndef HJ_MIN_CTAS
+#define HJ_MIN_CTAS (512 / HJ_THREADS)
+#endif
+constexpr int kThreads = HJ_THREADS;
+constexpr int kCtasPerSm = HJ_MIN_CTAS;
+// Strip widths (MCUs per CTA) so one sweep step has ~kThreads two-block jobs:
+// 444 -> ceil(S/2) + S, 422 -> S + (S+2), 420 -> 2S + (S+2).
+constexpr int kStrip444 = (2 * kThreads) / 3;
+constexpr int kStrip422 = (kThreads - 2) / 2;
+constexpr int kStrip420 = (kThreads - 2) / 3;
 
 inline int strip_width(int sub) {
     return sub == HJ_SUB_444 ? kStrip444 : sub == HJ_SUB_422 ? kStrip422 : kStrip420;
