@@ -1,0 +1,4 @@
+timeout 400 python -m pytest tests -m gpu -x -q --timeout 120 > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+tail -3 gpurun_out/pytest_gpu.log | cut -c1-600
+for w in 1080p420 4096p444 4096p422 24mp420; do timeout 120 python bench.py --workload $w --steps 300 --no-cpu-baseline --e2e-steps 1 2>>gpurun_out/bench.err | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$w', d['value'], d['roofline']['frac'], d['idct_screen'], d['e2e']['bit_exact_vs_oracle'])"; done
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:render_kernel -s 3 -c 1 -o gpurun_out/prof5 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_full5.log 2>&1; echo ncu rc=$?

@@ -122,22 +122,22 @@ __device__ __forceinline__ float4 lds128f(const float *p) {
 }
 
 // Per-sample rounding test of one f32x2 output pair (DESIGN.md "FP32
-// screen").  v is clamped below at -128.4 (every true sample below -128.4+E
-// rounds to 0 anyway), then t = v + C with C = 384.5 -/+ Eq lands in the
-// binade [256, 512) (ulp 2^-15) for v < 127.5, where floor(v + 128.5) =
+// screen").  t = v + C with C = 384.5 -/+ Eq lands in the binade [256, 512)
+// (ulp 2^-15) for v in [-128.5, 127.5), where floor(v + 128.5) =
 // (bits >> 15) - 0x8700.  `acc` collects bits(t-) ^ bits(t+): any bit >= 15
-// means some bracket straddles a rounding boundary (or a binade edge).
-// v >= 127.5 gives t >= 512, n >= 256 and a saturated 255 - correct, since
-// then the true sample exceeds 255.5 - E.
+// means some bracket straddles a rounding boundary or a binade edge.
+// Outside the binade the integer read-out saturates the right way with an
+// ARITHMETIC shift of the signed bit pattern: t >= 512 gives n >= 256 (255 -
+// the true sample exceeds 255.5 - E); 0 <= t < 256 gives n < 0 and a negative
+// t (v < -384.5) a negative pattern, both 0 - the true sample is below
+// -0.5 + E.  So no clamp is needed.
 __device__ __forceinline__ void round_pair(u64 v, u64 cm, u64 cp, uint32_t &acc, int &n_lo, int &n_hi) {
-    float lo = fmaxf(plo(v), -128.4f), hi = fmaxf(phi(v), -128.4f);
-    u64 w = pk(lo, hi);
-    u64 tm = add2(w, cm), tp = add2(w, cp);
+    u64 tm = add2(v, cm), tp = add2(v, cp);
     uint32_t a0 = __float_as_uint(plo(tm)), a1 = __float_as_uint(phi(tm));
     uint32_t b0 = __float_as_uint(plo(tp)), b1 = __float_as_uint(phi(tp));
     acc |= (a0 ^ b0) | (a1 ^ b1);
-    n_lo = (int)(a0 >> 15) - 0x8700;
-    n_hi = (int)(a1 >> 15) - 0x8700;
+    n_lo = ((int)a0 >> 15) - 0x8700;
+    n_hi = ((int)a1 >> 15) - 0x8700;
 }
 
 // FP32 screen of one block: returns true (and the 64 samples, u8 row-major,

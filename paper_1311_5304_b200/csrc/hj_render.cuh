@@ -20,13 +20,13 @@ struct Tile {
 };
 static_assert(sizeof(Tile) == 32, "Tile layout");
 
-// CTA size and residency (one CTA = one warp by default: warps sweep their
-// strips independently, synchronising only with warp barriers).
+// CTA size and residency: small CTAs (two warps) sweep their strips
+// independently, so barrier waits stay local to a strip.
 #ifndef HJ_THREADS
-#define HJ_THREADS 32
+#define HJ_THREADS 64
 #endif
 #ifndef HJ_MIN_CTAS
-#define HJ_MIN_CTAS (512 / HJ_THREADS)
+#define HJ_MIN_CTAS (384 / HJ_THREADS)  // 168 registers per thread: no spills
 #endif
 constexpr int kThreads = HJ_THREADS;
 constexpr int kCtasPerSm = HJ_MIN_CTAS;
