@@ -154,6 +154,16 @@ def peak_hbm():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(workload):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/traffic.json), or None when no capture exists."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return int(json.load(fh)[workload]["bytes"])
+    except Exception:
+        return None
+
+
 def cpu_baseline(images, wl, budget_s=3.0):
     """Oracle port on the host cores: bounded sample (>= budget_s wall)."""
     from oracle import oracle
@@ -316,7 +326,8 @@ def main():
                        "parallelism": f"image-sharded x{world}"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "frac": round(achieved / peak, 4),
+                         "traffic": ncu_traffic(args.workload) if args.batch == 0 else None,
                          "kernel_ms": round(kernel_ms, 5)},
             "e2e": {"value": round(e2e_value, 1), "unit": "Mpix/s",
                     "h2d_bytes_per_step": io["h2d_bytes"], "d2h_bytes_per_step": io["d2h_bytes"],
