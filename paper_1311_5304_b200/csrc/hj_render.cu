@@ -1,27 +1,34 @@
-// sm_100a render kernel: dequantise -> IDCT -> [h2v1 / h2v2 fancy upsample]
-// -> YCbCr->RGB, bit-exact against the reference's float64 path.
+// sm_100a render kernel (v3): dequantise -> IDCT -> [h2v1 / h2v2 fancy
+// upsample] -> YCbCr->RGB, bit-exact against the reference's float64 path
+// (kernels/_native.pyx:312-549, kernels/fallback.py:37-260).
 //
-// IDCT numerics:  every block is first transformed
-// in binary32 with the reference's AAN operation order, packed two columns /
-// two rows per f32x2 instruction (FFMA2/FADD2).  A rigorous first-order
-// error bound E = u * sum_i K_i |x_i| (K from tools/analysis/
-// screen_constants.py) brackets each sample; if no rounding boundary of
-// floor(s + 128.5) lies inside [s - E, s + E] for all 64 samples, the binary32
-// result provably rounds like the reference's float64 one.  Otherwise (a few
-// percent of real blocks, all blocks in "direct" mode) the block is queued and
-// recomputed in exact float64 (explicitly rounded __dadd_rn/__dmul_rn, the
-// reference's operation order) by the CTA's fallback pass.
+// IDCT numerics: every block is first transformed
+// in binary32 with the reference's AAN operation order.  A thread screens
+// TWO blocks at once, block A in the low and block B in the high lane of
+// every f32x2 register, so both 1-D passes run as FADD2/FFMA2 with no
+// register transposes.  A rigorous first-order error bound
+// E = u * sum_i K_i |x_i| (K from tools/analysis/screen_constants.py)
+// brackets each sample; if no rounding boundary of floor(s + 128.5) lies
+// inside [s - E, s + E] for all 64 samples, the binary32 result provably
+// rounds like the reference's float64 one.  Otherwise (a few percent of real
+// blocks; every block in "direct" mode) the block is queued and recomputed in
+// exact float64 (explicitly rounded __dadd_rn/__dmul_rn, the reference's
+// operation order) by 8 cooperating threads.
 //
-// Work decomposition: a CTA (128 threads) owns a strip of MCU columns of one
-// image and sweeps down a range of MCU rows.  Per MCU row:
-//   (1) screen: each thread takes one job of two blocks (two Y blocks, or
-//       the Cb+Cr pair of one MCU), writes Y samples as u8 and chroma as SWAR
-//       words (Cb | Cr << 16) so the upsampler filters both planes per op;
-//   (2) exact fallback for queued blocks (float64, few threads);
-//   (3) upsample + colour + store: 8 pixels per item, integer colour
-//       formulas, saturating I2IP byte packing, 8-byte RGB stores.
-// 4:2:2 / 4:2:0 strips include the chroma MCU left/right of the strip; 4:2:0
-// keeps the previous / next chroma MCU row resident (vertical context).
+// Work decomposition: a CTA (64 threads) owns a strip of MCU columns of one
+// image and sweeps down a range of MCU rows.  Step s is two phases:
+//   A. screen: one job (two blocks) per thread - the Y blocks of MCU row s
+//      and the chroma (Cb, Cr) pairs of MCU row s (s+1 for 4:2:0, whose
+//      vertical filter needs the next row) -> sample planes in shared memory;
+//      blocks the screen cannot prove are queued.
+//   B. the queued blocks' exact recompute, overlapped with the pixel stage
+//      of MCU row s-1 (16-pixel items handed out through a shared counter,
+//      so the threads busy with float64 simply take fewer items):
+//      upsample (SWAR, both chroma planes per 32-bit op) + integer colour +
+//      saturating I2IP byte packing + 16-byte RGB stores.
+// Sample planes are double (Y) / triple (4:2:0 chroma) buffered across steps.
+// One thread prefetches the next step's coefficient ranges into L2 with
+// bulk prefetches (cp.async.bulk.prefetch.L2).
 #include <cstdint>
 
 #include "hj_common.cuh"
@@ -114,6 +121,14 @@ __device__ __forceinline__ void aan_x2(u64 &d0, u64 &d1, u64 &d2, u64 &d3, u64 &
     d7 = sub2(e0, t7);
 }
 
+// Bracket constants of one block: E = u*B*(1 + 2.5e-3) + 2^-16 (rounding of
+// t) + 2^-30 (float64 side), rounded up to the 2^-15 grid so 384.5 -/+ Eq is
+// exact in binary32.
+__device__ __forceinline__ float bracket(float B) {
+    float e = fmaf(B, 5.9754e-8f, 1.5260e-5f);
+    return ceilf(e * 32768.0f) * (1.0f / 32768.0f);
+}
+
 __device__ __forceinline__ float4 lds128f(const float *p) {
     float4 v;
     unsigned a = (unsigned)__cvta_generic_to_shared(p);
@@ -173,9 +188,7 @@ __device__ __forceinline__ bool screen_block(const int16_t *__restrict__ src, co
     }
     // bound: E = u*B*(1 + 2.5e-3) + 2^-16 (rounding of t) + 2^-30 (float64
     // side), rounded up to the 2^-15 grid so 384.5 -/+ Eq is exact in binary32
-    float B = (b0 + b1) + (b2 + b3);
-    float e = fmaf(B, 5.9754e-8f, 1.5260e-5f);
-    float eq = ceilf(e * 32768.0f) * (1.0f / 32768.0f);
+    const float eq = bracket((b0 + b1) + (b2 + b3));
     u64 cm = pk(384.5f - eq, 384.5f - eq), cpl = pk(384.5f + eq, 384.5f + eq);
 
 #pragma unroll
@@ -210,7 +223,7 @@ __device__ __forceinline__ bool screen_block(const int16_t *__restrict__ src, co
 // l in the column pass, row l in the row pass), the reference's operation
 // order (_native.pyx:364-388); column results staged in `g` (64 doubles,
 // shared).  Returns row l's 8 rounded samples packed in a uint2.
-__device__ __forceinline__ uint2 exact_block_x8(const int16_t *__restrict__ src, const int *q, bool direct,
+__device__ __noinline__ uint2 exact_block_x8(const int16_t *__restrict__ src, const int *q, bool direct,
                                                 double *g, int l, unsigned mask) {
     {
         double d[8];
@@ -237,74 +250,238 @@ __device__ __forceinline__ uint2 exact_block_x8(const int16_t *__restrict__ src,
 
 // ------------------------------------------------------------- geometry
 
+// Chroma planes: 4:4:4 keeps Cb and Cr as byte planes (no filter).  4:2:2 /
+// 4:2:0 keep SWAR words (c_cb | c_cr << 16) << CSH so the fancy filters run
+// on both planes per 32-bit op; 4:2:0 scales by 16 and 4:2:2 by 64 so the
+// filtered values land in byte 1 / byte 3 of each word (every lane stays
+// below 2^16).  The 4:2:x chroma window covers MCUs [m0-1, m1+1).
 template <int SUB>
 struct Geo;
-// Chroma SWAR words hold (c << CSH) | (c << CSH) << 16: 4:2:0 scales by 16 and
-// 4:2:2 by 64 so the fancy filters' results land byte-aligned (the filtered
-// value is byte 1 / byte 3 of the word; every lane stays below 2^16).
 template <>
 struct Geo<HJ_SUB_444> {
     static constexpr int S = kStrip444, MW = 8, MH = 8, CSH = 0;
-    static constexpr int YW = 8 * S;   // Y plane width (bytes)
-    static constexpr int CW = 8 * S;   // chroma window width (words)
-    static constexpr int CROWS = 8;
+    static constexpr int YW = 8 * S;      // Y / Cb / Cr plane width (bytes)
+    static constexpr int CW = 0;
+    static constexpr int YSLOTS = 2;
+    static constexpr int CROWS = 0;
 };
 template <>
 struct Geo<HJ_SUB_422> {
     static constexpr int S = kStrip422, MW = 16, MH = 8, CSH = 6;
     static constexpr int YW = 16 * S;
-    static constexpr int CW = 8 * (S + 2);
-    static constexpr int CROWS = 8;
+    static constexpr int CW = 8 * (S + 2);  // SWAR window width (words)
+    static constexpr int YSLOTS = 2;
+    static constexpr int CROWS = 2 * 8;     // two slots of one MCU row
 };
 template <>
 struct Geo<HJ_SUB_420> {
     static constexpr int S = kStrip420, MW = 16, MH = 16, CSH = 4;
     static constexpr int YW = 16 * S;
     static constexpr int CW = 8 * (S + 2);
-    static constexpr int CROWS = 17;  // MCU rows c (slot c&1, 8 rows each) + row 16: last row of r-1
+    static constexpr int YSLOTS = 2;
+    static constexpr int CROWS = 3 * 8 + 1;  // three MCU-row slots + the saved last row (index 24)
 };
 
 constexpr int kExactGroups = kThreads / 8;  // blocks recomputed in parallel
-constexpr int kQueueMax = 2 * kThreads;     // >= blocks of one sweep step
+constexpr int kQueueMax = 2 * kThreads;     // >= blocks of one step
 
 template <int SUB>
 struct Smem {
     using G = Geo<SUB>;
-    uint8_t ys[G::MH * G::YW];
-    uint32_t cs[G::CROWS * G::CW];          // SWAR chroma: Cb | Cr << 16
-    float qf[3][64];                        // binary32 q * pre (screen)
+    alignas(16) uint8_t ys[G::YSLOTS][G::MH * G::YW];
+    // 4:4:4: Cb, Cr byte planes (two slots); 4:2:x: SWAR chroma rows
+    alignas(16) uint8_t cbp[SUB == HJ_SUB_444 ? 2 : 1][SUB == HJ_SUB_444 ? 8 * G::YW : 16];
+    alignas(16) uint8_t crp[SUB == HJ_SUB_444 ? 2 : 1][SUB == HJ_SUB_444 ? 8 * G::YW : 16];
+    alignas(16) uint32_t cs[SUB == HJ_SUB_444 ? 1 : G::CROWS][SUB == HJ_SUB_444 ? 4 : G::CW];
+    alignas(16) float qf[3][64];            // binary32 q * pre (screen)
     int qi[3][64];                          // integer q (exact path)
     double g[kExactGroups][64];             // exact-path column results
-    uint32_t queue[kQueueMax];              // exact-path jobs
-    uint32_t qdst[kQueueMax];
-    uint4 cscratch[kThreads][4];            // Cb samples of a chroma job
-    int n_queue[2];                         // per iteration parity (reset lag)
+    uint32_t queue[2][kQueueMax];           // exact-path jobs: comp << 30 | block
+    uint32_t qdst[2][kQueueMax];            // destination (see push_exact)
+    int n_queue[2];
+    int n_taken[2];                         // pixel-item counters
 };
 
-__device__ __forceinline__ void write_y_rows(uint8_t *ys, int yoff, int stride, const uint32_t (&w)[16]) {
+__device__ __forceinline__ void sts128(void *p, uint4 v) { *reinterpret_cast<uint4 *>(p) = v; }
+__device__ __forceinline__ uint4 lds128(const void *p) { return *reinterpret_cast<const uint4 *>(p); }
+
+__device__ __forceinline__ void write_block_rows(uint8_t *dst, int stride, const uint32_t (&a)[16]) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-        *reinterpret_cast<uint2 *>(ys + yoff + r * stride) = make_uint2(w[2 * r], w[2 * r + 1]);
+    for (int r = 0; r < 8; ++r) *reinterpret_cast<uint2 *>(dst + r * stride) = make_uint2(a[2 * r], a[2 * r + 1]);
 }
 
-// Interleave Cb and Cr sample rows into SWAR words:
-// word k = (cb_k | cr_k << 16) << CSH.
+// SWAR chroma rows: word k = (cb_k | cr_k << 16) << CSH, 8 words per row.
 template <int CSH>
-__device__ __forceinline__ void write_c_rows(uint32_t *cs, int coff, int stride, const uint4 *cb,
-                                             const uint32_t (&cr)[16]) {
+__device__ __forceinline__ void write_swar_rows(uint32_t *cs, int stride, const uint32_t (&cb)[16],
+                                                const uint32_t (&cr)[16]) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-        uint4 cbv = cb[r >> 1];
-        const uint32_t cbw[2] = {(r & 1) ? cbv.z : cbv.x, (r & 1) ? cbv.w : cbv.y};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            uint32_t a = cbw[h], b = cr[2 * r + h];
-            uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
-            uint4 v = make_uint4(__byte_perm(t0, 0, 0x4140) << CSH, __byte_perm(t0, 0, 0x4342) << CSH,
-                                 __byte_perm(t1, 0, 0x4140) << CSH, __byte_perm(t1, 0, 0x4342) << CSH);
-            *reinterpret_cast<uint4 *>(cs + coff + r * stride + 4 * h) = v;
+            const uint32_t a = cb[2 * r + h], b = cr[2 * r + h];
+            const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+            sts128(cs + r * stride + 4 * h,
+                   make_uint4(__byte_perm(t0, 0, 0x4140) << CSH, __byte_perm(t0, 0, 0x4342) << CSH,
+                              __byte_perm(t1, 0, 0x4140) << CSH, __byte_perm(t1, 0, 0x4342) << CSH));
         }
     }
+}
+
+// Destination encoding of a queued exact block: bits 31-30 = kind
+// (0: byte plane offset, 2: SWAR Cb lane, 3: SWAR Cr lane), low 30 bits =
+// byte offset into the Smem struct (byte planes) or word index (SWAR).
+__device__ __forceinline__ void push_exact(int *n_queue, uint32_t *queue, uint32_t *qdst, uint32_t job,
+                                           uint32_t dst) {
+    const int e = atomicAdd(n_queue, 1);
+    queue[e] = job;
+    qdst[e] = dst;
+}
+
+// Unaligned / cropped tail of a 16-pixel RGB row (rare: odd widths, right edge).
+__device__ __noinline__ void store_partial(uint8_t *__restrict__ dst, uint4 a, uint4 b, uint4 c, int nbytes) {
+    const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int i = 0; i < 48; ++i)
+        if (i < nbytes) dst[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+}
+
+// Pixel items are handed out 32 at a time per warp (one shared atomic per
+// warp and round), so warps busy with exact blocks take fewer rounds.
+__device__ __forceinline__ int grab32(int *taken) {
+    int base = 0;
+    if ((threadIdx.x & 31) == 0) base = atomicAdd(taken, 32);
+    return __shfl_sync(0xffffffffu, base, 0) + (threadIdx.x & 31);
+}
+
+// Colour + pack of 4 pixels (Y bytes of `yw`, chroma ints) -> 12 RGB bytes
+// in 3 words.  Small live ranges on purpose: the colour constants stay in
+// registers instead of being rematerialised per pixel.
+__device__ __forceinline__ void colour4(uint32_t yw, int cb0, int cr0, int cb1, int cr1, int cb2, int cr2,
+                                        int cb3, int cr3, bool &special, uint32_t &w0, uint32_t &w1,
+                                        uint32_t &w2) {
+    const Rgb p0 = colour((int)__byte_perm(yw, 0, 0x4440), cb0, cr0, special);
+    const Rgb p1 = colour((int)__byte_perm(yw, 0, 0x4441), cb1, cr1, special);
+    const Rgb p2 = colour((int)__byte_perm(yw, 0, 0x4442), cb2, cr2, special);
+    const Rgb p3 = colour((int)__byte_perm(yw, 0, 0x4443), cb3, cr3, special);
+    w0 = pack4(p0.r, p0.g, p0.b, p1.r);
+    w1 = pack4(p1.g, p1.b, p2.r, p2.g);
+    w2 = pack4(p2.b, p3.r, p3.g, p3.b);
+}
+
+__device__ __forceinline__ void store48(uint8_t *__restrict__ dst, const uint32_t (&w)[12], int npx) {
+    if (npx == 16 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        uint4 *d = reinterpret_cast<uint4 *>(dst);
+        d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        d[2] = make_uint4(w[8], w[9], w[10], w[11]);
+    } else if (npx == 16 && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+        uint32_t *d = reinterpret_cast<uint32_t *>(dst);
+#pragma unroll
+        for (int i = 0; i < 12; ++i) d[i] = w[i];
+    } else {
+        store_partial(dst, make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]),
+                      make_uint4(w[8], w[9], w[10], w[11]), npx * 3);
+    }
+}
+
+// Rare path: the 16 pixels held the float64 tie pair (Cb, Cr) = (78, 178)
+// (SURVEY.md E3): recompute them with the exact G rule and store.  Inputs by
+// value (no local arrays on the hot path).  is444: a = Cb bytes, b = Cr
+// bytes; else a, b, e = the 10 SWAR chroma sums of render16_swar.
+__device__ __noinline__ void render16_exact(uint8_t *__restrict__ dst, uint4 yv, uint4 a, uint4 b, uint2 e,
+                                            uint32_t rnd_e, uint32_t rnd_o, int is444, int npx) {
+    const uint32_t yw[4] = {yv.x, yv.y, yv.z, yv.w};
+    int cb[16], cr[16];
+    if (is444) {
+        const uint32_t bw[4] = {a.x, a.y, a.z, a.w}, rw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            cb[i] = (int)((bw[i >> 2] >> (8 * (i & 3))) & 0xff);
+            cr[i] = (int)((rw[i >> 2] >> (8 * (i & 3))) & 0xff);
+        }
+    } else {
+        const uint32_t c[10] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, e.x, e.y};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t t3 = c[i + 1] * 3u;
+            const uint32_t ev = t3 + c[i] + rnd_e, od = t3 + c[i + 2] + rnd_o;
+            cb[2 * i] = (int)((ev >> 8) & 0xff);
+            cr[2 * i] = (int)(ev >> 24);
+            cb[2 * i + 1] = (int)((od >> 8) & 0xff);
+            cr[2 * i + 1] = (int)(od >> 24);
+        }
+    }
+    uint32_t w[12];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        Rgb p[4];
+        bool dummy = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = 4 * q + k, y = (int)((yw[q] >> (8 * k)) & 0xff);
+            p[k] = colour(y, cb[i], cr[i], dummy);
+            p[k].g = colour_g_exact(y, cb[i], cr[i]);
+        }
+        w[3 * q] = pack4(p[0].r, p[0].g, p[0].b, p[1].r);
+        w[3 * q + 1] = pack4(p[1].g, p[1].b, p[2].r, p[2].g);
+        w[3 * q + 2] = pack4(p[2].b, p[3].r, p[3].g, p[3].b);
+    }
+    store48(dst, w, npx);
+}
+
+// 16 pixels of a 4:2:x row: Y bytes `yv`, chroma SWAR sums c[0..9] (c[1..8]
+// under the 16 pixels), horizontal fancy filter even = 3c + prev + rnd_e,
+// odd = 3c + next + rnd_o with the result in byte 1 (Cb) / byte 3 (Cr) of
+// each lane; colour; 48 bytes stored at dst (cropped to npx).
+__device__ __forceinline__ void render16_swar(uint8_t *__restrict__ dst, uint4 yv, const uint32_t (&c)[10],
+                                              uint32_t rnd_e, uint32_t rnd_o, int npx) {
+    const uint32_t yw[4] = {yv.x, yv.y, yv.z, yv.w};
+    uint32_t w[12];
+    bool special = false;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t ta = c[2 * q + 1] * 3u, tb = c[2 * q + 2] * 3u;
+        const uint32_t e0 = ta + c[2 * q] + rnd_e, o0 = ta + c[2 * q + 2] + rnd_o;
+        const uint32_t e1 = tb + c[2 * q + 1] + rnd_e, o1 = tb + c[2 * q + 3] + rnd_o;
+        colour4(yw[q], (int)__byte_perm(e0, 0, 0x4441), (int)(e0 >> 24), (int)__byte_perm(o0, 0, 0x4441),
+                (int)(o0 >> 24), (int)__byte_perm(e1, 0, 0x4441), (int)(e1 >> 24),
+                (int)__byte_perm(o1, 0, 0x4441), (int)(o1 >> 24), special, w[3 * q], w[3 * q + 1], w[3 * q + 2]);
+    }
+    if (special) {
+        render16_exact(dst, yv, make_uint4(c[0], c[1], c[2], c[3]), make_uint4(c[4], c[5], c[6], c[7]),
+                       make_uint2(c[8], c[9]), rnd_e, rnd_o, 0, npx);
+        return;
+    }
+    store48(dst, w, npx);
+}
+
+// 16 pixels of a 4:4:4 row from Y / Cb / Cr byte vectors.
+__device__ __forceinline__ void render16_444(uint8_t *__restrict__ dst, uint4 yv, uint4 bv, uint4 rv, int npx) {
+    const uint32_t yw[4] = {yv.x, yv.y, yv.z, yv.w}, bw[4] = {bv.x, bv.y, bv.z, bv.w},
+                   rw[4] = {rv.x, rv.y, rv.z, rv.w};
+    uint32_t w[12];
+    bool special = false;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        colour4(yw[q], (int)(bw[q] & 0xff), (int)((rw[q]) & 0xff), (int)__byte_perm(bw[q], 0, 0x4441),
+                (int)__byte_perm(rw[q], 0, 0x4441), (int)__byte_perm(bw[q], 0, 0x4442),
+                (int)__byte_perm(rw[q], 0, 0x4442), (int)(bw[q] >> 24), (int)(rw[q] >> 24), special, w[3 * q],
+                w[3 * q + 1], w[3 * q + 2]);
+    if (special) {
+        render16_exact(dst, yv, bv, rv, make_uint2(0, 0), 0, 0, 1, npx);
+        return;
+    }
+    store48(dst, w, npx);
+}
+
+// 10 SWAR words of one chroma row: p[-1], p[0..7], p[8] with edge
+// replication at the padded plane's first / last column.
+__device__ __forceinline__ void load_c10(const uint32_t *p, bool left_edge, bool right_edge, uint32_t (&c)[10]) {
+    const uint4 m0 = lds128(p), m1 = lds128(p + 4);
+    c[1] = m0.x; c[2] = m0.y; c[3] = m0.z; c[4] = m0.w;
+    c[5] = m1.x; c[6] = m1.y; c[7] = m1.z; c[8] = m1.w;
+    c[0] = left_edge ? c[1] : p[-1];
+    c[9] = right_edge ? c[8] : p[8];
 }
 
 template <int SUB>
@@ -321,151 +498,165 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
     const int S = t.m1 - t.m0;
     const bool direct = (im.flags & HJ_FLAG_DIRECT_IDCT) != 0;
     for (int i = tid; i < 192; i += kThreads) {
-        int q = im.q[i];
+        const int q = im.q[i];
         sm.qi[i >> 6][i & 63] = q;
-        sm.qf[i >> 6][i & 63] = (float)((double)q * kPre64[i & 63]);
     }
-    if (tid == 0) sm.n_queue[0] = sm.n_queue[1] = 0;
+    for (int i = tid; i < 192; i += kThreads) sm.qf[i >> 6][i & 63] = (float)((double)im.q[i] * kPre64[i & 63]);
+    if (tid == 0) sm.n_queue[0] = sm.n_queue[1] = sm.n_taken[0] = sm.n_taken[1] = 0;
 
-    // chroma MCU window of the strip: [m0-1, m1+1) for 4:2:2/4:2:0
-    const int cm_lo = (SUB == HJ_SUB_444) ? t.m0 : t.m0 - 1;
+    const int cm_lo = (SUB == HJ_SUB_444) ? t.m0 : t.m0 - 1;  // first chroma window MCU
     const int n_cm = (SUB == HJ_SUB_444) ? S : S + 2;
-    // Y jobs: two blocks each (444: MCU pair; 422: one MCU; 420: half MCU)
+    // Y jobs (two blocks): 444 MCU pair; 422 one MCU; 420 half MCU
     const int n_yj = (SUB == HJ_SUB_444) ? (S + 1) / 2 : (SUB == HJ_SUB_422 ? S : 2 * S);
     const bool left_edge = (t.m0 == 0), right_edge = (t.m1 == mpr);
-    const int n_groups = (G::MW / 8) * S;  // 8-pixel groups per pixel row of the strip
-    const int oy0 = tid / n_groups, gx0 = tid - oy0 * n_groups;
-    const int ystep = kThreads / n_groups, gstep = kThreads - ystep * n_groups;
+    constexpr int YB = G::MW / 8 * (G::MH / 8);          // Y blocks per MCU
+    const int mcu_rows = im.mcu_rows;
     __syncthreads();
 
-    // One transform job = two blocks through one screen call site, kept
-    // branch-free up to the call so a warp mixing Y and chroma jobs runs the
-    // screen once per block slot (no divergent duplication).  Y job: blocks
-    // side by side in the Y plane; chroma job (job >= n_yj): the Cb and Cr
-    // block of one MCU of chroma row crow, combined into SWAR words.
-    // Exact-path queue entry: comp << 30 | block index; destination: Y byte
-    // offset, or 1 << 31 | lane << 30 | chroma word offset.
-    auto run_job = [&](int job, int yrow, int crow, int *n_queue, bool active) {
-        const bool is_y = job < n_yj;
-        const int lm = job - n_yj;                 // chroma window MCU
-        const int m = cm_lo + lm;
-        const bool valid = active && (is_y || (m >= 0 && m < mpr));
-        const int nb = (SUB == HJ_SUB_444 && is_y && 2 * job + 1 >= S) ? 1 : 2;
-        // Y: first block index and plane offset of the job
-        int64_t yblk;
-        int yoff0;
-        if (SUB == HJ_SUB_444) {
-            yblk = (int64_t)yrow * mpr + t.m0 + 2 * job;
-            yoff0 = 2 * job * 8;
-        } else if (SUB == HJ_SUB_422) {
-            yblk = ((int64_t)yrow * mpr + t.m0 + job) * 2;
-            yoff0 = job * 16;
-        } else {  // MCU job/2, blocks 0,1 (top) or 2,3 (bottom)
-            yblk = ((int64_t)yrow * mpr + t.m0 + (job >> 1)) * 4 + 2 * (job & 1);
-            yoff0 = (job & 1) * 8 * G::YW + (job >> 1) * 16;
-        }
-        const int64_t cblk = (int64_t)crow * mpr + m;
-        const int coff = (SUB == HJ_SUB_420 ? (crow & 1) * 8 * G::CW : 0) + lm * 8;
-        if constexpr (SUB == HJ_SUB_420) {
-            // copy-on-overwrite: the slot's old row 7 (chroma MCU row crow-2)
-            // becomes row 16, the context of MCU row crow-1
-            if (valid && !is_y) {
-#pragma unroll
-                for (int i = 0; i < 8; i += 4)
-                    *reinterpret_cast<uint4 *>(sm.cs + 16 * G::CW + lm * 8 + i) =
-                        *reinterpret_cast<const uint4 *>(sm.cs + coff + 7 * G::CW + i);
-            }
-        }
-        // the same job of the next iteration reads the blocks one MCU row
-        // down: pull them into L2 now (hides DRAM latency next iteration)
-        if (valid) {
-            const bool more = is_y ? (yrow + 1 < t.r1) : (crow + 1 < im.mcu_rows && crow + 1 <= t.r1);
-            if (more) {
-                const int64_t ystep = (int64_t)mpr * (G::MW / 8) * (G::MH / 8);  // Y blocks per MCU row
-                const int16_t *p0 = is_y ? im.y + (yblk + ystep) * 64 : im.cb + (cblk + mpr) * 64;
-                const int16_t *p1 = is_y ? p0 + 64 : im.cr + (cblk + mpr) * 64;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(p0));
-                if (nb > 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(p1));
-            }
-        }
-        bool ok0 = false;
+    // step range: 4:2:0 screens chroma one MCU row ahead (vertical context)
+    const int s_begin = (SUB == HJ_SUB_420) ? max(t.r0 - 2, -1) : t.r0;
+    const int s_end = t.r1;  // the last step only draws row r1-1
 #pragma unroll 1
-        for (int k = 0; k < 2; ++k) {
-            const bool run = valid && k < nb;
-            const int64_t blk = is_y ? yblk + k : cblk;
-            const int16_t *src = (is_y ? im.y : (k == 0 ? im.cb : im.cr)) + blk * 64;
-            const float *qf = sm.qf[is_y ? 0 : 1 + k];
-            uint32_t w[16];
-            bool ok = false;
-            if (run) ok = !direct && screen_block(src, qf, w);
-            if (!run) continue;
-            if (is_y) {
-                const int yoff = yoff0 + k * 8;
-                if (ok) {
-                    write_y_rows(sm.ys, yoff, G::YW, w);
-                } else {
-                    int e = atomicAdd(n_queue, 1);
-                    sm.queue[e] = (uint32_t)blk;
-                    sm.qdst[e] = (uint32_t)yoff;
-                }
-            } else if (k == 0) {
-                ok0 = ok;
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    sm.cscratch[tid][i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
-            } else if (ok && ok0) {
-                write_c_rows<G::CSH>(sm.cs, coff, G::CW, sm.cscratch[tid], w);
-            } else {
-                int e = atomicAdd(n_queue, 2);
-                sm.queue[e] = (uint32_t)blk | (1u << 30);
-                sm.qdst[e] = (uint32_t)coff | (1u << 31);
-                sm.queue[e + 1] = (uint32_t)blk | (2u << 30);
-                sm.qdst[e + 1] = (uint32_t)coff | (1u << 31) | (1u << 30);
+    for (int s = s_begin; s <= s_end; ++s) {
+        const int par = s & 1;
+        int *const nq = &sm.n_queue[par];
+        uint32_t *const queue = sm.queue[par];
+        uint32_t *const qdst = sm.qdst[par];
+        const bool do_y = s >= t.r0 && s < t.r1;
+        const int crow = (SUB == HJ_SUB_420) ? s + 1 : s;
+        const bool do_c = (SUB == HJ_SUB_420) ? (crow >= t.r0 - 1 && crow <= t.r1 && crow >= 0 && crow < mcu_rows)
+                                              : do_y;
+        if (tid == 0) {
+            sm.n_queue[par ^ 1] = 0;  // last used in step s-1, next in s+1
+            sm.n_taken[par ^ 1] = 0;
+            // bulk L2 prefetch of the next step's coefficient ranges
+            const int ny = s + 1;
+            if (ny >= t.r0 && ny < t.r1) {
+                const int64_t b0 = ((int64_t)ny * mpr + t.m0) * YB;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(im.y + b0 * 64),
+                             "r"((unsigned)(S * YB * 128)));
+            }
+            const int nc = crow + 1;
+            if (nc < mcu_rows && nc <= t.r1) {
+                const int c0 = max(cm_lo, 0), c1 = min(cm_lo + n_cm, mpr);
+                const int64_t b0 = (int64_t)nc * mpr + c0;
+                const unsigned bytes = (unsigned)((c1 - c0) * 128);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(im.cb + b0 * 64), "r"(bytes));
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(im.cr + b0 * 64), "r"(bytes));
             }
         }
-    };
 
-    // 4:2:0 sweeps one iteration ahead on chroma: iteration `it` transforms
-    // the Y blocks of MCU row it and the chroma of MCU row it+1, starting two
-    // iterations early (transform-only) to bring in rows r0-1 and r0.
-    const int it0 = (SUB == HJ_SUB_420) ? max(t.r0 - 2, -1) : t.r0;
+        // ---------------- phase A: screen (one two-block job per thread)
+        {
+            const int n_y = do_y ? n_yj : 0;
+            const int n_jobs = n_y + (do_c ? n_cm : 0);
 #pragma unroll 1
-    for (int it = it0; it < t.r1; ++it) {
-        const bool draw = it >= t.r0;
-        int crow = it, n_c = n_cm;
-        if (SUB == HJ_SUB_420) {
-            crow = it + 1;
-            n_c = (crow >= t.r0 - 1 && crow >= 0 && crow < im.mcu_rows) ? n_cm : 0;
-        }
-        const int n_y = draw ? n_yj : 0;
-        // ---- (1) binary32 screen of this iteration's blocks
-        int *const nq = &sm.n_queue[it & 1];
-        // every lane runs the job loop the same number of times (inactive
-        // lanes ride along) so the screen is never split by divergence
-        const int n_jobs = n_y + n_c;
+            for (int j = tid; j < n_jobs; j += kThreads) {
+                const bool is_y = j < n_y;
+                const int lm = j - n_y;            // chroma window MCU
+                const int m = cm_lo + lm;
+                if (!is_y && (m < 0 || m >= mpr)) continue;
+                const int16_t *srcA, *srcB;
+                bool has_b = true;
+                uint32_t dA, dB;                   // exact-path destinations
+                uint8_t *ydst = nullptr;           // Y-like byte rows
+                uint32_t *cdst = nullptr;          // SWAR rows
+                int cw0 = 0;
+                if (is_y) {
+                    int64_t yblk;
+                    int yoff;
+                    if (SUB == HJ_SUB_444) {
+                        yblk = (int64_t)s * mpr + t.m0 + 2 * j;
+                        yoff = 16 * j;
+                        has_b = 2 * j + 1 < S;
+                    } else if (SUB == HJ_SUB_422) {
+                        yblk = ((int64_t)s * mpr + t.m0 + j) * 2;
+                        yoff = 16 * j;
+                    } else {
+                        yblk = ((int64_t)s * mpr + t.m0 + (j >> 1)) * 4 + 2 * (j & 1);
+                        yoff = (j & 1) * 8 * G::YW + (j >> 1) * 16;
+                    }
+                    srcA = im.y + yblk * 64;
+                    srcB = has_b ? srcA + 64 : srcA;
+                    ydst = sm.ys[par] + yoff;
+                    dA = (uint32_t)(ydst - smem_raw);
+                    dB = dA + 8;
+                } else {
+                    const int64_t cblk = (int64_t)crow * mpr + m;
+                    srcA = im.cb + cblk * 64;
+                    srcB = im.cr + cblk * 64;
+                    if (SUB == HJ_SUB_444) {
+                        ydst = sm.cbp[par] + 8 * lm;
+                        dA = (uint32_t)(ydst - smem_raw);
+                        dB = (uint32_t)(sm.crp[par] + 8 * lm - smem_raw);
+                    } else {
+                        const int slot = (SUB == HJ_SUB_420) ? (crow % 3) : par;
+                        cw0 = slot * 8 * G::CW + 8 * lm;
+                        cdst = &sm.cs[0][0] + cw0;
+                        dA = (2u << 30) | (uint32_t)cw0;
+                        dB = (3u << 30) | (uint32_t)cw0;
+                        if constexpr (SUB == HJ_SUB_420) {
+                            // the slot's old row 7 (MCU row crow-3) is the top
+                            // context of MCU row crow-2, drawn this step
+                            uint32_t *save = &sm.cs[24][0] + 8 * lm;
+                            const uint32_t *old = cdst + 7 * G::CW;
+                            sts128(save, lds128(old));
+                            sts128(save + 4, lds128(old + 4));
+                        }
+                    }
+                }
+                // the two blocks through one (rolled) screen call site; block
+                // A's samples stay in `keep` until B is done
+                uint32_t keep[16];
+                bool okA = false;
+                if (has_b && !direct) asm volatile("prefetch.global.L1 [%0];" ::"l"(srcB));
 #pragma unroll 1
-        for (int j0 = 0; j0 < n_jobs; j0 += kThreads) {
-            const int j = j0 + tid;
-            run_job(j < n_y ? j : n_yj + (j - n_y), it, crow, nq, j < n_jobs);
+                for (int k = 0; k < 2; ++k) {
+                    if (k == 1 && !has_b) break;
+                    uint32_t w[16];
+                    const int comp = is_y ? 0 : 1 + k;
+                    bool ok = false;
+                    if (!direct) ok = screen_block(k ? srcB : srcA, sm.qf[comp], w);
+                    if (SUB == HJ_SUB_444 || is_y) {
+                        // byte planes: Y (blocks side by side) or Cb / Cr
+                        uint8_t *dst = is_y ? ydst + 8 * k : (k ? sm.crp[par] + 8 * lm : ydst);
+                        if (!direct) write_block_rows(dst, G::YW, w);
+                        if (!ok) {
+                            const int64_t blk = ((k ? srcB : srcA) - (is_y ? im.y : k ? im.cr : im.cb)) / 64;
+                            push_exact(nq, queue, qdst, ((uint32_t)comp << 30) | (uint32_t)blk, k ? dB : dA);
+                        }
+                    } else if (k == 0) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) keep[i] = w[i];
+                        okA = ok;
+                    } else {
+                        if (!direct) write_swar_rows<G::CSH>(cdst, G::CW, keep, w);
+                        const uint32_t blk = (uint32_t)((int64_t)crow * mpr + m);
+                        if (!okA) push_exact(nq, queue, qdst, (1u << 30) | blk, dA);
+                        if (!ok) push_exact(nq, queue, qdst, (2u << 30) | blk, dB);
+                    }
+                }
+            }
         }
         __syncthreads();
-        // ---- (2) exact float64 recompute of the unproven blocks, 8 threads each
+
+        // ---------------- phase B: exact recompute of this step's queue ...
         {
             const int n = *nq;
             const int grp = tid >> 3, l = tid & 7;
             const unsigned gmask = 0xffu << (tid & 24);  // the 8 lanes of this group
 #pragma unroll 1
             for (int e = grp; e < n; e += kExactGroups) {
-                const uint32_t job = sm.queue[e], dst = sm.qdst[e];
+                const uint32_t job = queue[e], dst = qdst[e];
                 const int comp = job >> 30;
                 const int64_t blk = job & 0x3fffffff;
                 const int16_t *src = (comp == 0 ? im.y : comp == 1 ? im.cb : im.cr) + blk * 64;
                 const uint2 row = exact_block_x8(src, sm.qi[comp], direct, sm.g[grp], l, gmask);
-                if (!(dst >> 31)) {
-                    *reinterpret_cast<uint2 *>(sm.ys + dst + l * G::YW) = row;
-                } else {
-                    const int coff = dst & 0x3fffffff, lane = (dst >> 30) & 1;
-                    uint16_t *c16 = reinterpret_cast<uint16_t *>(sm.cs + coff + l * G::CW) + lane;
+                const uint32_t kind = dst >> 30, off = dst & 0x3fffffff;
+                if (kind == 0) {
+                    *reinterpret_cast<uint2 *>(smem_raw + off + l * G::YW) = row;
+                } else if constexpr (SUB != HJ_SUB_444) {
+                    uint16_t *c16 = reinterpret_cast<uint16_t *>(&sm.cs[0][0] + off + l * G::CW) + (kind & 1);
 #pragma unroll
                     for (int c = 0; c < 8; ++c)
                         c16[2 * c] = (uint16_t)(((c < 4 ? row.x >> (8 * c) : row.y >> (8 * (c - 4))) & 0xff) << G::CSH);
@@ -473,110 +664,102 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
             }
             if (tid == 0 && n) atomicAdd(&g_exact_blocks, (unsigned long long)n);
         }
-        __syncthreads();
-        // this parity's counter is next used two iterations (>= 2 barriers) later
-        if (tid == 0) *nq = 0;
-        if (!draw) continue;
 
-        // ---- (3) upsample + colour + store MCU row `it`
-        const int y_base = it * G::MH;
-        const int x_base = t.m0 * G::MW;
-        const int ylim = min(G::MH, im.height - y_base);
-        // items (oy, gx) = 8 pixels, walked without a division per item
-        int oy = oy0, gx = gx0;
+        // ---------------- ... overlapped with the pixel stage of MCU row s-1
+        const int R = s - 1;
+        if (R >= t.r0 && R < t.r1) {
+            const int y_base = R * G::MH;
+            const int x_base = t.m0 * G::MW;
+            const uint8_t *yp = sm.ys[par ^ 1];
+            int *const taken = &sm.n_taken[par];
+            if constexpr (SUB == HJ_SUB_420) {
+                // item = (MCU column g, row pair p): output rows y_base+2p, +1
+                const int n_items = 8 * S;
+                const int gw = S;
+                const float inv_w = 1.0f / (float)gw;
+                const uint32_t *cnear = &sm.cs[0][0] + (R % 3) * 8 * G::CW;
+                const uint32_t *cnext = &sm.cs[0][0] + ((R + 1) % 3) * 8 * G::CW;
+                // top context of the MCU row's first sample row: the last row
+                // of MCU row R-1 - saved in row 24 when this step's chroma
+                // jobs overwrote its slot, else still in the slot
+                const uint32_t *cprev = do_c ? &sm.cs[24][0] : &sm.cs[0][0] + (((R + 2) % 3) * 8 + 7) * G::CW;
 #pragma unroll 1
-        for (; oy < ylim; gx += gstep, oy += ystep) {
-            if (gx >= n_groups) {
-                gx -= n_groups;
-                ++oy;
-                if (oy >= ylim) break;
-            }
-            const int x0 = x_base + gx * 8;
-            const int npx = min(8, im.width - x0);
-            if (npx <= 0) continue;
-            const uint2 yv = *reinterpret_cast<const uint2 *>(sm.ys + oy * G::YW + gx * 8);
-            int Y[8], cbv[8], crv[8];
+                for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
+                    const int i = i0;
+                    if (i >= n_items) continue;
+                    // row-major items: adjacent lanes store adjacent 48-byte runs
+                    const int p = __float2int_rd(((float)i + 0.5f) * inv_w), g = i - p * S;
+                    const int y0 = y_base + 2 * p;
+                    if (y0 >= im.height) continue;
+                    const int x0 = x_base + 16 * g;
+                    const int npx = min(16, im.width - x0);
+                    if (npx <= 0) continue;
+                    const int kw = 8 * (g + 1);  // window word of the MCU's chroma column 0
+                    const uint32_t *pn = cnear + p * G::CW + kw;
+                    const uint32_t *pu = p > 0 ? pn - G::CW : (R > 0 ? cprev + kw : pn);
+                    const uint32_t *pd = p < 7 ? pn + G::CW : (R + 1 < mcu_rows ? cnext + kw : pn);
+                    const bool le = left_edge && g == 0, re = right_edge && g == S - 1;
+                    // colsum = 3*near + far per lane (libjpeg h2v2 fancy), 16x scaled
+                    uint32_t n3[10];
+                    load_c10(pn, le, re, n3);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                Y[i] = (int)__byte_perm(yv.x, 0, 0x4440 + i);
-                Y[4 + i] = (int)__byte_perm(yv.y, 0, 0x4440 + i);
-            }
-            if (SUB == HJ_SUB_444) {
-                const uint32_t *cr = sm.cs + oy * G::CW + gx * 8;
-                uint4 a = *reinterpret_cast<const uint4 *>(cr), b = *reinterpret_cast<const uint4 *>(cr + 4);
-                const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                    for (int k = 0; k < 10; ++k) n3[k] *= 3u;
+                    const int rows = min(2, im.height - y0);
+#pragma unroll 1
+                    for (int h = 0; h < rows; ++h) {
+                        uint32_t cs10[10];
+                        load_c10(h ? pd : pu, le, re, cs10);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    cbv[i] = (int)__byte_perm(w[i], 0, 0x4440);
-                    crv[i] = (int)__byte_perm(w[i], 0, 0x4442);
+                        for (int k = 0; k < 10; ++k) cs10[k] += n3[k];
+                        // even 16(3cs+prev+8), odd 16(3cs+next+7)
+                        render16_swar(im.rgb + ((int64_t)(y0 + h) * im.width + x0) * 3,
+                                      lds128(yp + (2 * p + h) * G::YW + 16 * g), cs10, 0x00800080u, 0x00700070u,
+                                      npx);
+                    }
+                }
+            } else if constexpr (SUB == HJ_SUB_422) {
+                // item = (MCU column g, row y): 16 pixels
+                const int n_items = 8 * S;
+                const int gw = S;
+                const float inv_w = 1.0f / (float)gw;
+                const uint32_t *crow0 = &sm.cs[0][0] + (par ^ 1) * 8 * G::CW;
+#pragma unroll 1
+                for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
+                    const int i = i0;
+                    if (i >= n_items) continue;
+                    const int y = __float2int_rd(((float)i + 0.5f) * inv_w), g = i - y * gw;
+                    const int yy = y_base + y;
+                    if (yy >= im.height) continue;
+                    const int x0 = x_base + 16 * g;
+                    const int npx = min(16, im.width - x0);
+                    if (npx <= 0) continue;
+                    uint32_t c10[10];
+                    load_c10(crow0 + y * G::CW + 8 * (g + 1), left_edge && g == 0, right_edge && g == S - 1, c10);
+                    // h2v1 on 64x-scaled lanes: even 64(3c+prev+1), odd 64(3c+next+2)
+                    render16_swar(im.rgb + ((int64_t)yy * im.width + x0) * 3, lds128(yp + y * G::YW + 16 * g),
+                                  c10, 0x00400040u, 0x00800080u, npx);
                 }
             } else {
-                // chroma samples k0-1 .. k0+4 (k0 = 8*m0 + 4*gx) as window-local
-                // words; the padded plane's first/last column is replicated
-                // (fallback.py:200-212, _native.pyx:477-480)
-                const int kl = 8 * (t.m0 - cm_lo) + 4 * gx;
-                const int dl = (left_edge && gx == 0) ? 0 : -1;
-                const int dr = (right_edge && gx == n_groups - 1) ? 3 : 4;
-                uint32_t c[6];
-                uint32_t rnd_e, rnd_o;
-                if (SUB == HJ_SUB_422) {
-                    const uint32_t *cr = sm.cs + oy * G::CW + kl;
-                    uint4 mid = *reinterpret_cast<const uint4 *>(cr);
-                    c[0] = cr[dl];
-                    c[1] = mid.x;
-                    c[2] = mid.y;
-                    c[3] = mid.z;
-                    c[4] = mid.w;
-                    c[5] = cr[dr];
-                    // h2v1 on 64x-scaled lanes: even 64(3c+prev+1), odd 64(3c+next+2)
-                    rnd_e = 0x00400040u;
-                    rnd_o = 0x00800080u;
-                } else {
-                    // near chroma row ci, far row cf (clamped to the padded plane)
-                    const int ch_img = 8 * im.mcu_rows;
-                    const int ci = 8 * it + (oy >> 1);
-                    const int cf = min(max(ci + ((oy & 1) ? 1 : -1), 0), ch_img - 1);
-                    // row 8*it-1: saved in row 16 when this iteration overwrote
-                    // its slot with MCU row it+1, else still in slot (it-1)&1
-                    const int rn = (it & 1) * 8 + (ci & 7);
-                    const int rf = cf >= 8 * it ? (((cf >> 3) & 1) * 8 + (cf & 7))
-                                 : (it + 1 < im.mcu_rows ? 16 : ((it - 1) & 1) * 8 + 7);
-                    const uint32_t *cn = sm.cs + rn * G::CW + kl;
-                    const uint32_t *cfp = sm.cs + rf * G::CW + kl;
-                    uint4 mn = *reinterpret_cast<const uint4 *>(cn), mf = *reinterpret_cast<const uint4 *>(cfp);
-                    // colsum = 3*near + far per lane (libjpeg h2v2 fancy), 16x scaled
-                    c[0] = cn[dl] * 3u + cfp[dl];
-                    c[1] = mn.x * 3u + mf.x;
-                    c[2] = mn.y * 3u + mf.y;
-                    c[3] = mn.z * 3u + mf.z;
-                    c[4] = mn.w * 3u + mf.w;
-                    c[5] = cn[dr] * 3u + cfp[dr];
-                    // even 16(3cs+prev+8), odd 16(3cs+next+7)
-                    rnd_e = 0x00800080u;
-                    rnd_o = 0x00700070u;
-                }
-                // filtered value = byte 1 (Cb) / byte 3 (Cr) of each word
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint32_t t3 = c[i + 1] * 3u;
-                    const uint32_t ev = t3 + c[i] + rnd_e, od = t3 + c[i + 2] + rnd_o;
-                    cbv[2 * i] = (int)__byte_perm(ev, 0, 0x4441);
-                    crv[2 * i] = (int)(ev >> 24);
-                    cbv[2 * i + 1] = (int)__byte_perm(od, 0, 0x4441);
-                    crv[2 * i + 1] = (int)(od >> 24);
+                // item = (MCU pair g, row y): 16 pixels
+                const int gw = (S + 1) / 2;
+                const int n_items = 8 * gw;
+                const float inv_w = 1.0f / (float)gw;
+                const uint8_t *cbp = sm.cbp[par ^ 1], *crp = sm.crp[par ^ 1];
+#pragma unroll 1
+                for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
+                    const int i = i0;
+                    if (i >= n_items) continue;
+                    const int y = __float2int_rd(((float)i + 0.5f) * inv_w), g = i - y * gw;
+                    const int yy = y_base + y;
+                    if (yy >= im.height) continue;
+                    const int x0 = x_base + 16 * g;
+                    const int npx = min(min(16, im.width - x0), 8 * (S - 2 * g));
+                    if (npx <= 0) continue;
+                    const int o = y * G::YW + 16 * g;
+                    render16_444(im.rgb + ((int64_t)yy * im.width + x0) * 3, lds128(yp + o), lds128(cbp + o),
+                                 lds128(crp + o), npx);
                 }
             }
-            Rgb p[8];
-            bool special = false;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) p[i] = colour(Y[i], cbv[i], crv[i], special);
-            if (special) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) p[i].g = colour_g_exact(Y[i], cbv[i], crv[i]);
-            }
-            uint32_t w[6];
-            pack_rgb8(p, w);
-            store_rgb8(im.rgb + ((int64_t)(y_base + oy) * im.width + x0) * 3, w, npx);
         }
         __syncthreads();
     }

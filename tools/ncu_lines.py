@@ -7,7 +7,7 @@ import sys
 
 out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+top = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 40
 data, fname, hdr = [], "?", None
 for r in csv.reader(io.StringIO(out)):
     if not r:
@@ -29,5 +29,6 @@ for r in csv.reader(io.StringIO(out)):
 tot = sum(d[0] for d in data) or 1
 ws = sum(d[1] for d in data) or 1
 print(f"{'inst%':>6} {'stall%':>6}  line")
-for d in sorted(data, reverse=True)[:top]:
+key = (lambda d: d[1]) if "--stall" in sys.argv else (lambda d: d[0])
+for d in sorted(data, key=key, reverse=True)[:top]:
     print(f"{d[0] / tot * 100:6.2f} {d[1] / ws * 100:6.2f}  {d[2]:22s} {d[3]}")
