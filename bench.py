@@ -58,6 +58,8 @@ def parse_args():
     ap.add_argument("--batch", type=int, default=0, help="images per GPU per step (0 = default)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-amdahl", action="store_true", help="skip the Huffman-inclusive pipeline run")
+    ap.add_argument("--amdahl-images", type=int, default=32, help="images per rank in the pipeline run")
     return ap.parse_args()
 
 
@@ -186,6 +188,39 @@ def cpu_baseline(images, wl, budget_s=3.0):
                       "(oracle/render_oracle.c, float64 AAN as the reference)"}
 
 
+def amdahl_run(images, wl, world, pg, n_images):
+    """Full decode of a batch (host Huffman on this rank's share of the host
+    cores, pipelined with H2D -> kernel -> D2H on the B200) against the
+    Huffman stage alone with the same decoder and threads:
+    frac = T_huff / T_wall = achieved fraction of the Amdahl-bound speedup
+    (orchestrator.py:71-75, §6.4)."""
+    from paper_1311_5304_b200.pipeline import BatchDecoder
+    threads = max(1, len(os.sched_getaffinity(0)) // world)
+    blobs = [images[i % len(images)][0] for i in range(n_images)]
+    dec = BatchDecoder(blobs, threads=threads, n_streams=4)
+    try:
+        dec.run()  # warm-up: plans, page-locked buffers
+        huff = [dec.huffman_only() for _ in range(3)]
+        walls = [dec.run()["wall_s"] for _ in range(3)]
+        from oracle import oracle
+        _, _, c0, q0 = images[0]
+        w, h = wl[0], wl[1]
+        want = oracle.render(c0.y_blocks, c0.cb_blocks, c0.cr_blocks, q0, w, h,
+                             {"444": 0, "422": 1, "420": 2}[wl[3]], True, threads)
+        exact = bool(np.array_equal(dec.pixels[0].data, want))
+    finally:
+        dec.close()
+    t_h = allreduce_max(pg, min(huff))
+    t_w = allreduce_max(pg, min(walls))
+    px = world * n_images * wl[0] * wl[1]
+    return {"t_huff_ms": round(t_h * 1e3, 3), "t_wall_ms": round(t_w * 1e3, 3),
+            "frac_of_bound": round(t_h / t_w, 4), "mpix_s": round(px / t_w / 1e6, 1),
+            "huffman_mpix_s": round(px / t_h / 1e6, 1), "host_threads_per_rank": threads,
+            "images_per_rank": n_images, "bit_exact_vs_oracle": exact,
+            "note": "T_huff = native host Huffman alone (same decoder/threads); T_wall = Huffman "
+                    "pipelined with H2D+render+D2H on 4 CUDA streams; min of 3 runs, max over ranks"}
+
+
 def run_reference(args, wl, world, rank, pg):
     if rank != 0:
         return
@@ -307,6 +342,11 @@ def main():
                          len(os.sched_getaffinity(0)))
     exact = bool(np.array_equal(out_arrays[0], want))
 
+    # ---- end to end INCLUDING host Huffman: the paper's Amdahl metric
+    amdahl = None
+    if not args.no_amdahl:
+        amdahl = amdahl_run(images, wl, world, pg, args.amdahl_images)
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(images, wl)
@@ -334,6 +374,7 @@ def main():
                     "steps": e2e_steps, "bit_exact_vs_oracle": exact},
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
+            "amdahl": amdahl,
             "idct_screen": {"exact_fp64_block_frac": round(
                 exact_blocks / (args.steps * sum(s.n_y + 2 * s.n_c for s in db.slots)), 5)},
             "clocks": clk,

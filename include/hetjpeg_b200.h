@@ -129,6 +129,18 @@ hj_status hj_render_rows(const int16_t *y, const int16_t *cb, const int16_t *cr,
                          int32_t subsampling, int32_t fast, int32_t fused,
                          int64_t n_y_blocks, int64_t n_c_blocks);
 
+/* hj_render_rows plus the device time of its three phases, measured with
+ * CUDA events on the library's stream: phase_ms[0] = H2D of the coefficient
+ * rows (+ plan), [1] = render kernel(s), [2] = D2H of the RGB rows.  This is
+ * what the accelerator lane reports where the reference's simulated lane
+ * sleeps (executors.py:163-187: write / compute / read). */
+hj_status hj_render_rows_timed(const int16_t *y, const int16_t *cb, const int16_t *cr,
+                               const int32_t *q3x64, uint8_t *rgb,
+                               int32_t width, int32_t height, int32_t mcus_per_row,
+                               int32_t mcu_rows, int32_t row0, int32_t n_rows,
+                               int32_t subsampling, int32_t fast, int32_t fused,
+                               int64_t n_y_blocks, int64_t n_c_blocks, float *phase_ms);
+
 /* Single-block transforms for the reference's per-block API
  * (block_transforms.py / fallback.py:103-119): n dequantised blocks
  * (int32, natural order) -> 64 samples each (uint8, +128, rounded, clamped),

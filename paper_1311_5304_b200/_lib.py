@@ -98,6 +98,8 @@ _SIG = {
     "hj_exact_block_count": (C.c_uint64, []),
     "hj_render_rows": (C.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
                                  _I32, _I32, _I64, _I64]),
+    "hj_render_rows_timed": (C.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32,
+                                       _I32, _I32, _I32, _I64, _I64, _P]),
     "hj_idct_blocks": (C.c_int, [_P, _I64, _P, _I32]),
     "hj_idct_blocks_f64": (C.c_int, [_P, _I64, _P, _I32]),
     "hj_ycbcr_to_rgb": (C.c_int, [_P, _P, _P, _P, _I64]),

@@ -166,14 +166,19 @@ struct SyncCtx {
     size_t rgb_bytes = 0;
     void *misc = nullptr;  // q (768 B) + image desc + tiles
     size_t misc_bytes = 0;
-    ~SyncCtx() {
+    std::vector<uint8_t> host_plan;  // staging of [image desc][tiles]
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    void release() {
         if (device >= 0) {
             cudaFree(coef);
             cudaFree(rgb);
             cudaFree(misc);
+            for (auto &e : ev)
+                if (e) cudaEventDestroy(e);
             if (stream) cudaStreamDestroy(stream);
         }
     }
+    ~SyncCtx() { release(); }
 };
 thread_local SyncCtx t_ctx;
 
@@ -194,13 +199,15 @@ hj_status ctx_get(SyncCtx **out) {
     SyncCtx &c = t_ctx;
     if (c.device != dev) {
         if (c.device >= 0) {
-            cudaFree(c.coef);
-            cudaFree(c.rgb);
-            cudaFree(c.misc);
-            if (c.stream) cudaStreamDestroy(c.stream);
-            c = SyncCtx();
+            c.release();
+            c.device = -1;
+            c.coef = c.rgb = c.misc = nullptr;
+            c.coef_bytes = c.rgb_bytes = c.misc_bytes = 0;
+            for (auto &e : c.ev) e = nullptr;
+            c.stream = nullptr;
         }
         HJ_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        for (auto &e : c.ev) HJ_CUDA(cudaEventCreate(&e));
         c.device = dev;
     }
     *out = &c;
@@ -332,12 +339,12 @@ uint64_t hj_launch_count(void) { return g_launches.load(); }
 
 uint64_t hj_exact_block_count(void) { return hj::exact_block_count(); }
 
-hj_status hj_render_rows(const int16_t *y, const int16_t *cb, const int16_t *cr,
-                         const int32_t *q3x64, uint8_t *rgb, int32_t width, int32_t height,
-                         int32_t mcus_per_row, int32_t mcu_rows, int32_t row0, int32_t n_rows,
-                         int32_t subsampling, int32_t fast, int32_t fused,
-                         int64_t n_y_blocks, int64_t n_c_blocks) {
-    (void)fused;  // fused and unfused paths are byte-identical (fallback.py:230-234)
+static hj_status render_rows_impl(const int16_t *y, const int16_t *cb, const int16_t *cr,
+                                  const int32_t *q3x64, uint8_t *rgb, int32_t width, int32_t height,
+                                  int32_t mcus_per_row, int32_t mcu_rows, int32_t row0, int32_t n_rows,
+                                  int32_t subsampling, int32_t fast, int64_t n_y_blocks, int64_t n_c_blocks,
+                                  float *phase_ms) {
+    if (phase_ms) phase_ms[0] = phase_ms[1] = phase_ms[2] = 0.f;
     if (n_rows <= 0) return HJ_OK;  // block_transforms.py:66-67
     if (!y || !cb || !cr || !q3x64 || !rgb) return fail(HJ_ERR_ARG, "null pointer");
     hj_image_t im{};
@@ -373,38 +380,74 @@ hj_status hj_render_rows(const int16_t *y, const int16_t *cb, const int16_t *cr,
     SyncCtx *c = nullptr;
     st = ctx_get(&c);
     if (st != HJ_OK) return st;
+    // tile list on the host; [q 1 KB][image desc][tiles] in one device buffer
+    std::vector<hj::Tile> tiles;
+    std::vector<Plan::Group> groups;
+    build_tiles(&im, 1, tiles, groups);
+    const size_t img_off = 1024, tile_off = 1024 + 256;
+    const size_t misc_need = tile_off + sizeof(hj::Tile) * tiles.size();
     const size_t coef_bytes = (size_t)(nyb + 2 * ncb) * 128;
     st = ensure(&c->coef, &c->coef_bytes, coef_bytes);
     if (st == HJ_OK) st = ensure(&c->rgb, &c->rgb_bytes, std::max<size_t>(rgb_bytes, 16));
-    // misc: q (768 B, 256-aligned slot) + plan image/tiles are built separately
-    if (st == HJ_OK) st = ensure(&c->misc, &c->misc_bytes, 1024);
+    if (st == HJ_OK) st = ensure(&c->misc, &c->misc_bytes, misc_need);
     if (st != HJ_OK) return st;
+    uint8_t *misc = static_cast<uint8_t *>(c->misc);
     int16_t *dy = static_cast<int16_t *>(c->coef);
     int16_t *dcb = dy + nyb * 64;
     int16_t *dcr = dcb + ncb * 64;
-    int32_t *dq = static_cast<int32_t *>(c->misc);
-    HJ_CUDA(cudaMemcpyAsync(dy, y + (int64_t)row0 * per_row_y * 64, nyb * 128, cudaMemcpyHostToDevice, c->stream));
-    HJ_CUDA(cudaMemcpyAsync(dcb, cb + (int64_t)c_lo * per_row_c * 64, ncb * 128, cudaMemcpyHostToDevice, c->stream));
-    HJ_CUDA(cudaMemcpyAsync(dcr, cr + (int64_t)c_lo * per_row_c * 64, ncb * 128, cudaMemcpyHostToDevice, c->stream));
-    HJ_CUDA(cudaMemcpyAsync(dq, q3x64, 768, cudaMemcpyHostToDevice, c->stream));
     // virtual bases so the kernel indexes whole-image block / pixel coordinates
     im.y = dy - (int64_t)row0 * per_row_y * 64;
     im.cb = dcb - (int64_t)c_lo * per_row_c * 64;
     im.cr = dcr - (int64_t)c_lo * per_row_c * 64;
-    im.q = dq;
+    im.q = reinterpret_cast<const int32_t *>(misc);
     im.rgb = static_cast<uint8_t *>(c->rgb) - (int64_t)py0 * width * 3;
-    Plan *p = nullptr;
-    st = plan_create(&im, 1, &p, c->stream);
-    if (st != HJ_OK) return st;
-    st = plan_launch(p, c->stream);
-    if (st == HJ_OK) {
-        cudaError_t e = cudaMemcpyAsync(rgb + (size_t)py0 * width * 3, c->rgb, rgb_bytes,
-                                        cudaMemcpyDeviceToHost, c->stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-        if (e != cudaSuccess) st = cuda_fail(e, "render_rows");
+    c->host_plan.resize(misc_need);
+    std::memcpy(c->host_plan.data(), q3x64, 768);
+    std::memcpy(c->host_plan.data() + img_off, &im, sizeof(im));
+    if (!tiles.empty()) std::memcpy(c->host_plan.data() + tile_off, tiles.data(), sizeof(hj::Tile) * tiles.size());
+
+    if (phase_ms) HJ_CUDA(cudaEventRecord(c->ev[0], c->stream));
+    HJ_CUDA(cudaMemcpyAsync(dy, y + (int64_t)row0 * per_row_y * 64, nyb * 128, cudaMemcpyHostToDevice, c->stream));
+    HJ_CUDA(cudaMemcpyAsync(dcb, cb + (int64_t)c_lo * per_row_c * 64, ncb * 128, cudaMemcpyHostToDevice, c->stream));
+    HJ_CUDA(cudaMemcpyAsync(dcr, cr + (int64_t)c_lo * per_row_c * 64, ncb * 128, cudaMemcpyHostToDevice, c->stream));
+    HJ_CUDA(cudaMemcpyAsync(misc, c->host_plan.data(), misc_need, cudaMemcpyHostToDevice, c->stream));
+    if (phase_ms) HJ_CUDA(cudaEventRecord(c->ev[1], c->stream));
+    const hj_image_t *dimg = reinterpret_cast<const hj_image_t *>(misc + img_off);
+    const hj::Tile *dtiles = reinterpret_cast<const hj::Tile *>(misc + tile_off);
+    for (const auto &g : groups) {
+        cudaError_t e = hj::launch_render(g.sub, g.direct, dimg, dtiles + g.offset, g.count, c->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "render kernel launch");
+        g_launches.fetch_add(1, std::memory_order_relaxed);
     }
-    hj_plan_destroy(p);
-    return st;
+    if (phase_ms) HJ_CUDA(cudaEventRecord(c->ev[2], c->stream));
+    HJ_CUDA(cudaMemcpyAsync(rgb + (size_t)py0 * width * 3, c->rgb, rgb_bytes, cudaMemcpyDeviceToHost, c->stream));
+    if (phase_ms) HJ_CUDA(cudaEventRecord(c->ev[3], c->stream));
+    HJ_CUDA(cudaStreamSynchronize(c->stream));
+    if (phase_ms) {
+        for (int k = 0; k < 3; ++k) HJ_CUDA(cudaEventElapsedTime(&phase_ms[k], c->ev[k], c->ev[k + 1]));
+    }
+    return HJ_OK;
+}
+
+hj_status hj_render_rows(const int16_t *y, const int16_t *cb, const int16_t *cr,
+                         const int32_t *q3x64, uint8_t *rgb, int32_t width, int32_t height,
+                         int32_t mcus_per_row, int32_t mcu_rows, int32_t row0, int32_t n_rows,
+                         int32_t subsampling, int32_t fast, int32_t fused,
+                         int64_t n_y_blocks, int64_t n_c_blocks) {
+    (void)fused;  // fused and unfused paths are byte-identical (fallback.py:230-234)
+    return render_rows_impl(y, cb, cr, q3x64, rgb, width, height, mcus_per_row, mcu_rows, row0, n_rows,
+                            subsampling, fast, n_y_blocks, n_c_blocks, nullptr);
+}
+
+hj_status hj_render_rows_timed(const int16_t *y, const int16_t *cb, const int16_t *cr,
+                               const int32_t *q3x64, uint8_t *rgb, int32_t width, int32_t height,
+                               int32_t mcus_per_row, int32_t mcu_rows, int32_t row0, int32_t n_rows,
+                               int32_t subsampling, int32_t fast, int32_t fused,
+                               int64_t n_y_blocks, int64_t n_c_blocks, float *phase_ms) {
+    (void)fused;
+    if (!phase_ms) return fail(HJ_ERR_ARG, "null phase_ms");
+    return render_rows_impl(y, cb, cr, q3x64, rgb, width, height, mcus_per_row, mcu_rows, row0, n_rows,
+                            subsampling, fast, n_y_blocks, n_c_blocks, phase_ms);
 }
 
 static hj_status run_blocks(const int32_t *deq, int64_t n, uint8_t *out, double *out_f64, int32_t fast) {

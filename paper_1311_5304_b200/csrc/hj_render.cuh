@@ -32,7 +32,7 @@ constexpr int kThreads = HJ_THREADS;
 constexpr int kCtasPerSm = HJ_MIN_CTAS;
 // Strip widths (MCUs per CTA) so one sweep step has ~kThreads two-block jobs:
 // 444 -> ceil(S/2) + S, 422 -> S + (S+2), 420 -> 2S + (S+2).
-constexpr int kStrip444 = (2 * kThreads) / 3;
+constexpr int kStrip444 = ((2 * kThreads) / 3) & ~1;  // even: 16-byte plane rows
 constexpr int kStrip422 = (kThreads - 2) / 2;
 constexpr int kStrip420 = (kThreads - 2) / 3;
 

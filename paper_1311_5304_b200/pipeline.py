@@ -63,3 +63,72 @@ def render_batch(coeffs, qtables, outs=None, chunk: int = 8, n_streams: int = 3)
     finally:
         lane.close()
     return outs
+
+
+class BatchDecoder:
+    """End-to-end batch decode: host Huffman on a thread pool (native C++,
+    GIL released) pipelined with the B200 parallel phase.
+
+    As each image's entropy decode finishes (into page-locked coefficient
+    buffers) the orchestrating thread queues H2D -> render -> D2H for it on
+    the next of `n_streams` CUDA streams, so the GPU work of finished images
+    overlaps the Huffman decoding of the rest - the paper's pipelined scheme
+    (§5.3) at batch granularity.  `huffman_only()` times the same
+    host stage alone (same decoder, same thread count): T_huff of the Amdahl
+    bound wall / huffman (orchestrator.py:71-75).
+    """
+
+    def __init__(self, blobs, threads: int = 0, n_streams: int = 4, fast: bool = True):
+        import os
+
+        from . import entropy, parser
+        from .block_transforms import alloc_pixels
+        from .perf_model import qtable_stack
+        self.threads = threads or len(os.sched_getaffinity(0))
+        self.blobs = [bytes(b) for b in blobs]
+        self.parsed = [parser.parse_stream(b) for b in self.blobs]
+        self.scans = [entropy.FastScan(p) for p in self.parsed]
+        self.geos = [s.geometry for s in self.scans]
+        self.q = [qtable_stack(p) for p in self.parsed]
+        self.coeffs = [entropy.alloc_coefficients(g, pinned=True) for g in self.geos]
+        self.pixels = [alloc_pixels(g.width, g.height, pinned=True) for g in self.geos]
+        self.batch = device.DeviceBatch(self.geos, fast=fast)
+        self.streams = [device.Stream() for _ in range(max(1, n_streams))]
+        for i in range(len(self.geos)):
+            self.batch.upload_qtables(i, self.q[i], self.streams[0])
+        self.streams[0].synchronize()
+
+    def _huff(self, i: int) -> int:
+        self.scans[i].decode(self.blobs[i], out=self.coeffs[i], threads=1)
+        return i
+
+    def huffman_only(self) -> float:
+        """Wall seconds of the host entropy stage alone over the batch."""
+        import time
+        from concurrent.futures import ThreadPoolExecutor
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(self.threads) as ex:
+            list(ex.map(self._huff, range(len(self.blobs))))
+        return time.perf_counter() - t0
+
+    def run(self) -> dict:
+        """Decode the whole batch into self.pixels; returns wall seconds and bytes moved."""
+        import time
+        from concurrent.futures import ThreadPoolExecutor, as_completed
+        b = self.batch
+        h2d = d2h = 0
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(self.threads) as ex:
+            futs = [ex.submit(self._huff, i) for i in range(len(self.blobs))]
+            for k, f in enumerate(as_completed(futs)):
+                i = f.result()
+                s = self.streams[k % len(self.streams)]
+                h2d += b.upload_coefficients(i, self.coeffs[i], s)
+                b.render_items([(i, 0, self.geos[i].mcu_rows)], s)
+                d2h += b.download_rgb(i, self.pixels[i].data, s)
+        for s in self.streams:
+            s.synchronize()
+        return {"wall_s": time.perf_counter() - t0, "h2d_bytes": h2d, "d2h_bytes": d2h}
+
+    def close(self):
+        self.batch.close()
