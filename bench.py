@@ -57,6 +57,7 @@ def parse_args():
     ap.add_argument("--workload", default="1080p420", choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=0, help="images per GPU per step (0 = default)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = auto")
+    ap.add_argument("--e2e-chunk", type=int, default=4, help="images per pipelined H2D/render/D2H chunk")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-amdahl", action="store_true", help="skip the Huffman-inclusive pipeline run")
     ap.add_argument("--amdahl-images", type=int, default=32, help="images per rank in the pipeline run")
@@ -319,7 +320,7 @@ def main():
     achieved = bytes_step / (kernel_ms / 1e3) / 1e9
 
     # ---- end to end through the public host API (pinned H2D -> kernel -> D2H)
-    lane = pipeline.GpuLane(geos, n_streams=3, chunk=8)
+    lane = pipeline.GpuLane(geos, chunk=args.e2e_chunk)
     from paper_1311_5304_b200.entropy import PinnedArray
     outs = [PinnedArray((g.height, g.width, 3), np.uint8) for g in geos]
     out_arrays = [o.array for o in outs]

@@ -87,6 +87,8 @@ hj_status hj_event_create(void **event);
 hj_status hj_event_destroy(void *event);
 hj_status hj_event_record(void *event, void *stream);
 hj_status hj_event_elapsed_ms(void *start, void *end, float *ms);
+/* Make `stream` wait (on the device) for `event` (cross-stream pipelining). */
+hj_status hj_stream_wait_event(void *stream, void *event);
 
 /* ---- the parallel phase: device-resident batch ---------------------- */
 /* Render every image of the batch on `stream` (asynchronous).  Replaces the

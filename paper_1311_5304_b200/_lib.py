@@ -90,6 +90,7 @@ _SIG = {
     "hj_event_destroy": (C.c_int, [_P]),
     "hj_event_record": (C.c_int, [_P, _P]),
     "hj_event_elapsed_ms": (C.c_int, [_P, _P, C.POINTER(C.c_float)]),
+    "hj_stream_wait_event": (C.c_int, [_P, _P]),
     "hj_render_batch": (C.c_int, [C.POINTER(hj_image_t), C.c_int, _P]),
     "hj_plan_create": (C.c_int, [C.POINTER(hj_image_t), C.c_int, C.POINTER(_P)]),
     "hj_plan_launch": (C.c_int, [_P, _P]),

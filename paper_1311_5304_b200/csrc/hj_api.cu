@@ -297,6 +297,10 @@ hj_status hj_event_record(void *event, void *stream) {
     HJ_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(event), as_stream(stream)));
     return HJ_OK;
 }
+hj_status hj_stream_wait_event(void *stream, void *event) {
+    HJ_CUDA(cudaStreamWaitEvent(as_stream(stream), reinterpret_cast<cudaEvent_t>(event), 0));
+    return HJ_OK;
+}
 hj_status hj_event_elapsed_ms(void *start, void *end, float *ms) {
     HJ_CUDA(cudaEventElapsedTime(ms, reinterpret_cast<cudaEvent_t>(start), reinterpret_cast<cudaEvent_t>(end)));
     return HJ_OK;

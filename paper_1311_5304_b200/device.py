@@ -46,6 +46,10 @@ class Stream:
     def synchronize(self):
         _lib.check(_lib.lib.hj_stream_synchronize(self.handle), "hj_stream_synchronize")
 
+    def wait(self, event: "Event") -> None:
+        """Device-side wait of this stream for `event`."""
+        _lib.check(_lib.lib.hj_stream_wait_event(self.handle, event.handle), "hj_stream_wait_event")
+
     def __del__(self):
         if getattr(self, "handle", None):
             _lib.lib.hj_stream_destroy(self.handle)
