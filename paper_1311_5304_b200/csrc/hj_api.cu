@@ -72,8 +72,8 @@ void build_tiles(const hj_image_t *images, int n, std::vector<hj::Tile> &tiles,
     int sms = 148;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t target = (int64_t)sms * hj::kCtasPerSm * 6;  // ~6 waves of resident CTAs
     for (int sub = HJ_SUB_444; sub <= HJ_SUB_420; ++sub) {
+        const int64_t target = (int64_t)sms * hj::ctas_per_sm(sub) * 6;  // ~6 waves of resident CTAs
         for (int direct = 0; direct < 2; ++direct) {
             int64_t strip_rows = 0;
             for (int i = 0; i < n; ++i) {

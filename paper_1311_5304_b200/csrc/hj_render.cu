@@ -282,8 +282,12 @@ struct Geo<HJ_SUB_420> {
     static constexpr int CROWS = 3 * 8 + 1;  // three MCU-row slots + the saved last row (index 24)
 };
 
-constexpr int kExactGroups = kThreads / 8;  // blocks recomputed in parallel
-constexpr int kQueueMax = 2 * kThreads;     // >= blocks of one step
+template <int SUB>
+constexpr int kNT = threads_for(SUB);           // threads per CTA
+template <int SUB>
+constexpr int kExactGroups = kNT<SUB> / 8;      // blocks recomputed in parallel
+template <int SUB>
+constexpr int kQueueMax = 2 * kNT<SUB>;         // >= blocks of one step
 
 template <int SUB>
 struct Smem {
@@ -295,9 +299,9 @@ struct Smem {
     alignas(16) uint32_t cs[SUB == HJ_SUB_444 ? 1 : G::CROWS][SUB == HJ_SUB_444 ? 4 : G::CW];
     alignas(16) float qf[3][64];            // binary32 q * pre (screen)
     int qi[3][64];                          // integer q (exact path)
-    double g[kExactGroups][64];             // exact-path column results
-    uint32_t queue[2][kQueueMax];           // exact-path jobs: comp << 30 | block
-    uint32_t qdst[2][kQueueMax];            // destination (see push_exact)
+    double g[kExactGroups<SUB>][64];        // exact-path column results
+    uint32_t queue[2][kQueueMax<SUB>];      // exact-path jobs: comp << 30 | block
+    uint32_t qdst[2][kQueueMax<SUB>];       // destination (see push_exact)
     int n_queue[2];
     int n_taken[2];                         // pixel-item counters
 };
@@ -485,7 +489,7 @@ __device__ __forceinline__ void load_c10(const uint32_t *p, bool left_edge, bool
 }
 
 template <int SUB>
-__global__ void __launch_bounds__(kThreads, HJ_MIN_CTAS)
+__global__ void __launch_bounds__(kNT<SUB>, ctas_per_sm(SUB))
 render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ tiles) {
     using G = Geo<SUB>;
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -497,6 +501,8 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
     const int mpr = im.mcus_per_row;
     const int S = t.m1 - t.m0;
     const bool direct = (im.flags & HJ_FLAG_DIRECT_IDCT) != 0;
+    constexpr int kThreads = kNT<SUB>;
+    constexpr int kExactGroups = ::hj::kExactGroups<SUB>;
     for (int i = tid; i < 192; i += kThreads) {
         const int q = im.q[i];
         sm.qi[i >> 6][i & 63] = q;
@@ -775,7 +781,7 @@ cudaError_t launch_sub(const hj_image_t *images, const Tile *tiles, int n_tiles,
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    render_kernel<SUB><<<n_tiles, kThreads, bytes, stream>>>(images, tiles);
+    render_kernel<SUB><<<n_tiles, kNT<SUB>, bytes, stream>>>(images, tiles);
     return cudaGetLastError();
 }
 

@@ -20,21 +20,28 @@ struct Tile {
 };
 static_assert(sizeof(Tile) == 32, "Tile layout");
 
-// CTA size and residency: small CTAs (two warps) sweep their strips
-// independently, so barrier waits stay local to a strip.
+// CTA size and residency: small CTAs sweep their strips independently, so
+// barrier waits stay local to a strip.  4:2:0 uses 4-warp CTAs (its wider
+// per-step pixel work balances the float64 fallback better), 4:4:4 / 4:2:2
+// 2-warp CTAs; 168 registers per thread, no spills.
+#ifndef HJ_THREADS_420
+#define HJ_THREADS_420 128
+#endif
 #ifndef HJ_THREADS
 #define HJ_THREADS 64
 #endif
-#ifndef HJ_MIN_CTAS
-#define HJ_MIN_CTAS (384 / HJ_THREADS)  // 168 registers per thread: no spills
-#endif
-constexpr int kThreads = HJ_THREADS;
-constexpr int kCtasPerSm = HJ_MIN_CTAS;
-// Strip widths (MCUs per CTA) so one sweep step has ~kThreads two-block jobs:
+constexpr int threads_for(int sub) { return sub == HJ_SUB_420 ? HJ_THREADS_420 : HJ_THREADS; }
+constexpr int ctas_per_sm(int sub) { return 384 / threads_for(sub); }
+// Strip widths (MCUs per CTA) so one sweep step has ~threads two-block jobs:
 // 444 -> ceil(S/2) + S, 422 -> S + (S+2), 420 -> 2S + (S+2).
-constexpr int kStrip444 = ((2 * kThreads) / 3) & ~1;  // even: 16-byte plane rows
-constexpr int kStrip422 = (kThreads - 2) / 2;
-constexpr int kStrip420 = (kThreads - 2) / 3;
+constexpr int strip_for(int sub) {
+    return sub == HJ_SUB_444 ? ((2 * threads_for(sub)) / 3) & ~1   // even: 16-byte plane rows
+         : sub == HJ_SUB_422 ? (threads_for(sub) - 2) / 2
+                             : (threads_for(sub) - 2) / 3;
+}
+constexpr int kStrip444 = strip_for(HJ_SUB_444);
+constexpr int kStrip422 = strip_for(HJ_SUB_422);
+constexpr int kStrip420 = strip_for(HJ_SUB_420);
 
 inline int strip_width(int sub) {
     return sub == HJ_SUB_444 ? kStrip444 : sub == HJ_SUB_422 ? kStrip422 : kStrip420;
