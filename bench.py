@@ -59,6 +59,10 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = auto")
     ap.add_argument("--e2e-chunk", type=int, default=4, help="images per pipelined H2D/render/D2H chunk")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="images", choices=["images", "rows"],
+                    help="N>1: images = each rank its own batch (weak scaling); rows = every rank "
+                         "renders its MCU-row range of the SAME images (strong scaling, "
+                         "BASELINE config 4; 4:2:0 ranks also load one chroma MCU row of context)")
     ap.add_argument("--no-amdahl", action="store_true", help="skip the Huffman-inclusive pipeline run")
     ap.add_argument("--amdahl-images", type=int, default=32, help="images per rank in the pipeline run")
     return ap.parse_args()
@@ -89,6 +93,15 @@ def allreduce_max(pg, value: float) -> float:
 def barrier(pg):
     if pg is not None:
         pg.barrier()
+
+
+def allreduce_sum(pg, value: float) -> float:
+    if pg is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64)
+    pg.all_reduce(t, op=pg.ReduceOp.SUM)
+    return float(t.item())
 
 
 def make_inputs(wl, rank, batch):
@@ -277,21 +290,42 @@ def main():
         return
 
     from paper_1311_5304_b200 import _lib, device, pipeline
-    _lib.check(_lib.lib.hj_set_device(local), "set device")
+    n_dev = max(1, _lib.lib.hj_device_count())
+    # testing aid only: HJ_BENCH_SHARE_DEVICE=1 lets N ranks share fewer GPUs
+    dev = local % n_dev if os.environ.get("HJ_BENCH_SHARE_DEVICE") else local
+    _lib.check(_lib.lib.hj_set_device(dev), "set device")
     w, h, q, sub, rst, batch = wl
-    images = make_inputs(wl, rank, batch)
+    rows_mode = args.shard == "rows"
+    images = make_inputs(wl, 0 if rows_mode else rank, batch)
     geos = [images[i % len(images)][2].geometry for i in range(batch)]
     db = device.DeviceBatch(geos)
     stream = device.Stream()
+    g0 = geos[0]
+    if rows_mode:
+        from paper_1311_5304_b200 import shard
+        row0, n_rows = shard.split_rows(g0.mcu_rows, world)[rank]
+        c_lo, c_hi = (shard.chroma_context(row0, n_rows, g0.mcu_rows) if sub == "420"
+                      else (row0, row0 + n_rows))
+        items = [(i, row0, n_rows) for i in range(batch)]
+    else:
+        row0, n_rows, c_lo, c_hi = 0, g0.mcu_rows, 0, g0.mcu_rows
+        items = None
     for i in range(batch):
         _, _, c, qt = images[i % len(images)]
-        db.upload_coefficients(i, c, stream)
+        db.upload_coefficients(i, c, stream, row0=c_lo, n_rows=c_hi - c_lo)
         db.upload_qtables(i, qt, stream)
     stream.synchronize()
+    y_lo, y_hi = row0 * g0.mcu_height, min(g0.height, (row0 + n_rows) * g0.mcu_height)
 
     # ---- kernel-only throughput (inputs resident in HBM)
+    def render_step():
+        if rows_mode:
+            db.render_items(items, stream)
+        else:
+            db.render(stream=stream)
+
     for _ in range(args.warmup):
-        db.render(stream=stream)
+        render_step()
     stream.synchronize()
     e0, e1 = device.Event(), device.Event()
     clocks = ClockSampler(local)
@@ -303,7 +337,7 @@ def main():
     exact0 = _lib.lib.hj_exact_block_count()
     e0.record(stream)
     for _ in range(args.steps):
-        db.render(stream=stream)
+        render_step()
     e1.record(stream)
     stream.synchronize()
     launches = _lib.lib.hj_launch_count() - launches0
@@ -312,9 +346,16 @@ def main():
     barrier(pg)
     ms = e0.elapsed_ms(e1)
     ms_max = allreduce_max(pg, ms)
-    px_step = db.pixels()
-    bytes_step = db.algorithmic_bytes()
-    value = world * px_step * args.steps / (ms_max / 1e3) / 1e6
+    if rows_mode:
+        px_step = batch * g0.width * (y_hi - y_lo)
+        bytes_step = batch * (n_rows * g0.mcus_per_row * (g0.y_blocks_per_mcu + 2) * 128
+                              + 3 * g0.width * (y_hi - y_lo))  # WorkItem.write_bytes + read_bytes
+        px_all = allreduce_sum(pg, px_step)
+    else:
+        px_step = db.pixels()
+        bytes_step = db.algorithmic_bytes()
+        px_all = world * px_step
+    value = px_all * args.steps / (ms_max / 1e3) / 1e6
     kernel_ms = ms / args.steps  # one launch per step (single subsampling family)
     peak, peak_kind = peak_hbm()
     achieved = bytes_step / (kernel_ms / 1e3) / 1e9
@@ -327,21 +368,47 @@ def main():
     coeffs = [images[i % len(images)][2] for i in range(batch)]
     qts = [images[i % len(images)][3] for i in range(batch)]
     e2e_steps = args.e2e_steps or max(3, min(20, args.steps // 100))
+
+    def e2e_step():
+        if not rows_mode:
+            return lane.run(coeffs, qts, out_arrays)
+        # this rank's MCU-row shard of every image: H2D (+ chroma context),
+        # render, D2H of its RGB rows, on the lane's three event-joined streams
+        b, h2d, d2h = lane.batch, 0, 0
+        for k0 in range(0, batch, lane.chunk):
+            idx = range(k0, min(batch, k0 + lane.chunk))
+            for i in idx:
+                h2d += b.upload_coefficients(i, coeffs[i], lane.h2d, row0=c_lo, n_rows=c_hi - c_lo)
+            ev_up, ev_done = device.Event(), device.Event()
+            ev_up.record(lane.h2d)
+            lane.comp.wait(ev_up)
+            b.render_items([(i, row0, n_rows) for i in idx], lane.comp)
+            ev_done.record(lane.comp)
+            lane.d2h.wait(ev_done)
+            for i in idx:
+                d2h += b.download_rgb(i, out_arrays[i], lane.d2h, y0=y_lo, y1=y_hi)
+        for st in lane.streams:
+            st.synchronize()
+        return {"h2d_bytes": h2d, "d2h_bytes": d2h}
+
+    if rows_mode:
+        for i in range(batch):
+            lane.batch.upload_qtables(i, qts[i], lane.h2d)
     for _ in range(2):
-        io = lane.run(coeffs, qts, out_arrays)
+        io = e2e_step()
     barrier(pg)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        io = lane.run(coeffs, qts, out_arrays)
+        io = e2e_step()
     e2e_s = allreduce_max(pg, time.perf_counter() - t0)
-    e2e_value = world * px_step * e2e_steps / e2e_s / 1e6
+    e2e_value = px_all * e2e_steps / e2e_s / 1e6
     # the e2e output must be the kernel's output: spot-check one image against the oracle
     from oracle import oracle
     _, _, c0, q0 = images[0]
     want = oracle.render(c0.y_blocks, c0.cb_blocks, c0.cr_blocks, q0, w, h,
                          {"444": 0, "422": 1, "420": 2}[sub], True,
                          len(os.sched_getaffinity(0)))
-    exact = bool(np.array_equal(out_arrays[0], want))
+    exact = bool(np.array_equal(out_arrays[0][y_lo:y_hi], want[y_lo:y_hi]))
 
     # ---- end to end INCLUDING host Huffman: the paper's Amdahl metric
     amdahl = None
@@ -357,14 +424,15 @@ def main():
             "metric": "decoded Mpix/s (parallel phase: dequant+IDCT+upsample+colour)",
             "value": round(value, 1), "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if rows_mode else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{w}x{h} {sub} q{q}" + (" rst" if rst else ""),
                        "images_per_step_per_gpu": batch, "distinct_images": len(images),
                        "bytes_per_step_per_gpu": bytes_step,
                        "l2": "inputs > L2 (coefficients %.0f MB/step/GPU)" % (
                            sum(s.coef_bytes for s in db.slots) / 1e6),
-                       "parallelism": f"image-sharded x{world}"},
+                       "parallelism": (f"MCU-row-sharded x{world} (rows {row0}..{row0 + n_rows - 1} "
+                                       "on rank 0)" if rows_mode else f"image-sharded x{world}")},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
@@ -377,7 +445,8 @@ def main():
             "gpu_launches": int(launches),
             "amdahl": amdahl,
             "idct_screen": {"exact_fp64_block_frac": round(
-                exact_blocks / (args.steps * sum(s.n_y + 2 * s.n_c for s in db.slots)), 5)},
+                exact_blocks / (args.steps * (batch * n_rows * g0.mcus_per_row * (g0.y_blocks_per_mcu + 2)
+                                              if rows_mode else sum(s.n_y + 2 * s.n_c for s in db.slots))), 5)},
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
