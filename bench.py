@@ -170,6 +170,25 @@ def peak_hbm():
         return 6650.0, "fallback"
 
 
+def issue_roofline(workload, value_mpix, sm_mhz, n_gpus):
+    """Second roofline: the render kernel is issue-bound.
+    thread-instructions per pixel from the committed ncu capture against the
+    SM array's issue rate (148 SMs x 4 schedulers x 32 lanes x clock)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            e = json.load(fh)[workload]
+        ipp = e["warp_instructions"] * 32 / e["pixels"]
+    except Exception:
+        return None
+    if not sm_mhz:
+        return None
+    ceiling = n_gpus * 148 * 4 * 32 * sm_mhz * 1e6 / ipp / 1e6
+    return {"thread_instr_per_px": round(ipp, 2), "issue_ceiling_mpix_s": round(ceiling, 1),
+            "frac": round(value_mpix / ceiling, 4),
+            "issue_slots_busy_pct_ncu": e.get("issue_slots_busy_pct"),
+            "source": e.get("report")}
+
+
 def ncu_traffic(workload):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     capture (profiles/traffic.json), or None when no capture exists."""
@@ -444,6 +463,8 @@ def main():
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "amdahl": amdahl,
+            "issue_roofline": issue_roofline(args.workload, value, clk.get("sm_mhz"), world)
+            if args.batch == 0 and not rows_mode else None,
             "idct_screen": {"exact_fp64_block_frac": round(
                 exact_blocks / (args.steps * (batch * n_rows * g0.mcus_per_row * (g0.y_blocks_per_mcu + 2)
                                               if rows_mode else sum(s.n_y + 2 * s.n_c for s in db.slots))), 5)},
