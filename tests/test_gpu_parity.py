@@ -205,3 +205,42 @@ def test_device_batch_mixed_subsamplings(cuda):
     s.synchronize()
     for c, o in zip(cases, outs):
         assert np.array_equal(o, c.rgb), c.name
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_mcu_row_sharding_with_only_local_coefficients(cuda, world):
+    """BASELINE config 4: one large 4:2:0 image with restart intervals split
+    into contiguous MCU-row shards, each 'rank' holding ONLY its rows plus
+    one chroma MCU row of context on each side (shard.chroma_context) on its
+    own device batch; the stitched RGB equals the oracle's whole-image render."""
+    from paper_1311_5304_b200 import device, entropy, parser, shard
+    from paper_1311_5304_b200.perf_model import qtable_stack
+    from paper_1311_5304_b200.synth import synth_jpeg
+    blob = synth_jpeg(1200, 800, 90, "420", seed=5, restart_rows=1)
+    p = parser.parse_stream(blob)
+    c, _ = entropy.decode_all(p, blob, pinned=True)
+    q = qtable_stack(p)
+    g = c.geometry
+    want = oracle.render(c.y_blocks, c.cb_blocks, c.cr_blocks, q, g.width, g.height, 2)
+    got = np.zeros_like(want)
+    s = device.Stream()
+    for row0, n in shard.split_rows(g.mcu_rows, world):
+        lo, hi = shard.chroma_context(row0, n, g.mcu_rows)
+        db = device.DeviceBatch([g])
+        _lib_memset_poison(db)
+        db.upload_coefficients(0, c, s, row0=lo, n_rows=hi - lo)
+        db.upload_qtables(0, q, s)
+        db.render_items([(0, row0, n)], s)
+        y0, y1 = row0 * 16, min(g.height, (row0 + n) * 16)
+        db.download_rgb(0, got, s, y0=y0, y1=y1)
+        s.synchronize()
+        db.close()
+    assert np.array_equal(got, want)
+
+
+def _lib_memset_poison(db):
+    """Fill the device coefficients with a pattern, so a shard reading rows it
+    does not own would change the output."""
+    from paper_1311_5304_b200 import _lib
+    _lib.check(_lib.lib.hj_memset_device(db.coef.ptr, 0x5A, db.coef.nbytes, None), "poison")
+    _lib.check(_lib.lib.hj_device_synchronize(), "sync")
