@@ -44,8 +44,13 @@ WORKLOADS = {
     "4096p444": (4096, 4096, 95, "444", 0, 8),
     "4096p422": (4096, 4096, 95, "422", 0, 8),
     "24mp420": (6000, 4000, 90, "420", 1, 8),
+    "1080p420q50": (1920, 1080, 50, "420", 0, 128),
+    "1080p444q50": (1920, 1080, 50, "444", 0, 128),
 }
 DISTINCT = 8  # distinct synthetic images per rank (replicated to the batch size)
+# "mixed" (BASELINE configs[4], scaled down): a seeded manifest of images of
+# 0.3-24 MP, four aspect ratios, q50-95, all three subsamplings, partitioned
+# over ranks by LPT on predicted cost (shard.assign_lpt)
 
 
 def parse_args():
@@ -54,7 +59,8 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="1080p420", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="1080p420", choices=sorted(WORKLOADS) + ["mixed"])
+    ap.add_argument("--mixed-images", type=int, default=24, help="images in the mixed manifest (all ranks)")
     ap.add_argument("--batch", type=int, default=0, help="images per GPU per step (0 = default)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = auto")
     ap.add_argument("--e2e-chunk", type=int, default=4, help="images per pipelined H2D/render/D2H chunk")
@@ -297,8 +303,128 @@ def run_reference(args, wl, world, rank, pg):
     print(json.dumps(line), flush=True)
 
 
+def mixed_manifest(n, seed=1311):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        area = float(np.exp(rng.uniform(np.log(0.3e6), np.log(24e6))))
+        ax, ay = [(1, 1), (4, 3), (3, 2), (16, 9)][int(rng.integers(0, 4))]
+        h = int(round((area * ay / ax) ** 0.5 / 2)) * 2
+        w = int(round(area / h / 2)) * 2
+        if rng.integers(0, 2):
+            w, h = h, w
+        out.append((w, h, int(rng.integers(50, 96)), ["444", "422", "420"][int(rng.integers(0, 3))]))
+    return out
+
+
+def run_mixed(args, world, rank, local, pg):
+    """Kernel-only + e2e throughput over this rank's LPT share of the mixed
+    manifest (one launch per subsampling family present)."""
+    from paper_1311_5304_b200 import _lib, device, entropy, parser, pipeline, shard
+    from paper_1311_5304_b200.perf_model import qtable_stack
+    from paper_1311_5304_b200.synth import synth_jpeg
+    n_dev = max(1, _lib.lib.hj_device_count())
+    _lib.check(_lib.lib.hj_set_device(local % n_dev if os.environ.get("HJ_BENCH_SHARE_DEVICE") else local),
+               "set device")
+    man = mixed_manifest(args.mixed_images)
+    ypm = {"444": 1, "422": 2, "420": 4}
+    mh = {"444": 8, "422": 8, "420": 16}
+    mw = {"444": 8, "422": 16, "420": 16}
+
+    def alg_bytes(w, h, sub):  # the memory-bound kernel's cost model
+        mcus = -(-w // mw[sub]) * -(-h // mh[sub])
+        return mcus * (ypm[sub] + 2) * 128 + 3 * w * h
+
+    mine = shard.assign_lpt([alg_bytes(*m[:2], m[3]) for m in man], world)[rank]
+    imgs = []
+    for k in mine:
+        w, h, q, sub = man[k]
+        blob = synth_jpeg(w, h, q, sub, seed=k)
+        p = parser.parse_stream(blob)
+        c, _ = entropy.decode_all(p, blob, pinned=True)
+        imgs.append((c, qtable_stack(p), sub))
+    geos = [c.geometry for c, _, _ in imgs]
+    db = device.DeviceBatch(geos)
+    st = device.Stream()
+    for i, (c, q, _) in enumerate(imgs):
+        db.upload_coefficients(i, c, st)
+        db.upload_qtables(i, q, st)
+    st.synchronize()
+    for _ in range(args.warmup):
+        db.render(stream=st)
+    st.synchronize()
+    e0, e1 = device.Event(), device.Event()
+    clocks = ClockSampler(local)
+    barrier(pg)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = _lib.lib.hj_launch_count()
+    x0 = _lib.lib.hj_exact_block_count()
+    e0.record(st)
+    for _ in range(args.steps):
+        db.render(stream=st)
+    e1.record(st)
+    st.synchronize()
+    launches = _lib.lib.hj_launch_count() - l0
+    exact_blocks = _lib.lib.hj_exact_block_count() - x0
+    clk = clocks.stop()
+    ms_max = allreduce_max(pg, e0.elapsed_ms(e1))
+    px_all = allreduce_sum(pg, db.pixels())
+    bytes_all = allreduce_sum(pg, db.algorithmic_bytes())
+    value = px_all * args.steps / (ms_max / 1e3) / 1e6
+    peak, peak_kind = peak_hbm()
+    achieved = bytes_all / world / (ms_max / args.steps / 1e3) / 1e9  # per GPU
+    lane = pipeline.GpuLane(geos, chunk=2)
+    outs = [entropy.PinnedArray((g.height, g.width, 3), np.uint8) for g in geos]
+    arrs = [o.array for o in outs]
+    cs, qs = [c for c, _, _ in imgs], [q for _, q, _ in imgs]
+    for _ in range(2):
+        io = lane.run(cs, qs, arrs)
+    barrier(pg)
+    e2e_steps = args.e2e_steps or 5
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        io = lane.run(cs, qs, arrs)
+    e2e_s = allreduce_max(pg, time.perf_counter() - t0)
+    from oracle import oracle
+    c, q, sub = imgs[0]
+    g = c.geometry
+    want = oracle.render(c.y_blocks, c.cb_blocks, c.cr_blocks, q, g.width, g.height,
+                         {"444": 0, "422": 1, "420": 2}[sub], True, len(os.sched_getaffinity(0)))
+    exact = bool(np.array_equal(arrs[0], want))
+    lane.close()
+    db.close()
+    if rank == 0:
+        line = {
+            "metric": "decoded Mpix/s (parallel phase: dequant+IDCT+upsample+colour)",
+            "value": round(value, 1), "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"mixed manifest of {len(man)} images, 0.3-24 MP, q50-95, 444/422/420",
+                       "images_on_rank0": len(imgs), "partition": "LPT on algorithmic bytes",
+                       "parallelism": f"image-sharded x{world}"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None},
+            "e2e": {"value": round(px_all * e2e_steps / e2e_s / 1e6, 1), "unit": "Mpix/s",
+                    "h2d_bytes_per_step": io["h2d_bytes"], "d2h_bytes_per_step": io["d2h_bytes"],
+                    "steps": e2e_steps, "bit_exact_vs_oracle": exact},
+            "gpu_launches": int(launches), "clocks": clk,
+            "idct_screen": {"exact_fp64_blocks_per_step": round(exact_blocks / args.steps, 1)},
+        }
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
 def main():
     args = parse_args()
+    if args.workload == "mixed":
+        world, rank, local, pg = dist_setup()
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "mixed workload: use the per-config lines"}))
+            return
+        run_mixed(args, world, rank, local, pg)
+        return
     wl = list(WORKLOADS[args.workload])
     if args.batch:
         wl[5] = args.batch

@@ -65,6 +65,14 @@ struct Plan {
     int n_images = 0;
     struct Group { int sub; bool direct; int offset; int count; };
     std::vector<Group> groups;
+    // a batch mixing subsamplings launches one kernel per family; they are
+    // independent, so they run concurrently on forked streams
+    mutable std::vector<cudaStream_t> side;
+    mutable std::vector<cudaEvent_t> ev;  // [0] fork, [1..] joins
+    ~Plan() {
+        for (auto st : side) cudaStreamDestroy(st);
+        for (auto e : ev) cudaEventDestroy(e);
+    }
 };
 
 void build_tiles(const hj_image_t *images, int n, std::vector<hj::Tile> &tiles,
@@ -75,22 +83,31 @@ void build_tiles(const hj_image_t *images, int n, std::vector<hj::Tile> &tiles,
     for (int sub = HJ_SUB_444; sub <= HJ_SUB_420; ++sub) {
         const int64_t target = (int64_t)sms * hj::ctas_per_sm(sub) * 6;  // ~6 waves of resident CTAs
         for (int direct = 0; direct < 2; ++direct) {
+            // rows per tile: enough tiles for ~6 waves, but 4:2:0 tiles re-transform
+            // two chroma MCU rows of vertical context, so keep them >= 8 rows; a
+            // small batch first gets narrower strips (only 2 chroma MCUs of
+            // horizontal context each) before shorter tiles
+            const int t_min = 8;  // a tile pays one fill and one drain step
+            int S = hj::strip_width(sub);
             int64_t strip_rows = 0;
-            for (int i = 0; i < n; ++i) {
-                const hj_image_t &im = images[i];
-                if (im.subsampling != sub || ((im.flags & HJ_FLAG_DIRECT_IDCT) != 0) != (direct != 0)) continue;
-                int S = hj::strip_width(sub);
-                int ns = (im.mcus_per_row + S - 1) / S;
-                strip_rows += (int64_t)ns * im.n_rows;
+            int T = t_min;
+            for (;;) {
+                strip_rows = 0;
+                for (int i = 0; i < n; ++i) {
+                    const hj_image_t &im = images[i];
+                    if (im.subsampling != sub || ((im.flags & HJ_FLAG_DIRECT_IDCT) != 0) != (direct != 0)) continue;
+                    strip_rows += (int64_t)((im.mcus_per_row + S - 1) / S) * im.n_rows;
+                }
+                T = (int)std::min<int64_t>(64, std::max<int64_t>(t_min, (strip_rows + target - 1) / target));
+                if (strip_rows == 0 || strip_rows / T >= target / 3 || S <= 12) break;
+                S = (S + 1) / 2;
             }
             if (strip_rows == 0) continue;
-            int T = (int)std::min<int64_t>(64, std::max<int64_t>(1, (strip_rows + target - 1) / target));
             Plan::Group g{sub, direct != 0, (int)tiles.size(), 0};
             for (int i = 0; i < n; ++i) {
                 const hj_image_t &im = images[i];
                 if (im.subsampling != sub || ((im.flags & HJ_FLAG_DIRECT_IDCT) != 0) != (direct != 0)) continue;
-                int S = hj::strip_width(sub);
-                int ns = (im.mcus_per_row + S - 1) / S;
+                const int ns = (im.mcus_per_row + S - 1) / S;
                 for (int r = im.row0; r < im.row0 + im.n_rows; r += T) {
                     int r1 = std::min(im.row0 + im.n_rows, r + T);
                     for (int s = 0; s < ns; ++s) {
@@ -148,11 +165,30 @@ hj_status plan_launch(const Plan *p, cudaStream_t stream) {
     if (!p || !p->dev) return HJ_OK;
     const hj_image_t *imgs = reinterpret_cast<const hj_image_t *>(p->dev);
     const hj::Tile *tiles = reinterpret_cast<const hj::Tile *>(static_cast<uint8_t *>(p->dev) + p->tile_base);
-    for (const auto &g : p->groups) {
-        cudaError_t e = hj::launch_render(g.sub, g.direct, imgs, tiles + g.offset, g.count, stream);
+    const size_t ng = p->groups.size();
+    if (ng > 1 && p->side.size() + 1 < ng) {
+        while (p->side.size() + 1 < ng) {
+            cudaStream_t st;
+            HJ_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            p->side.push_back(st);
+        }
+        while (p->ev.size() < ng) {
+            cudaEvent_t e;
+            HJ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            p->ev.push_back(e);
+        }
+    }
+    if (ng > 1) HJ_CUDA(cudaEventRecord(p->ev[0], stream));
+    for (size_t k = 0; k < ng; ++k) {
+        const auto &g = p->groups[k];
+        cudaStream_t st = k == 0 ? stream : p->side[k - 1];
+        if (k > 0) HJ_CUDA(cudaStreamWaitEvent(st, p->ev[0], 0));
+        cudaError_t e = hj::launch_render(g.sub, g.direct, imgs, tiles + g.offset, g.count, st);
         if (e != cudaSuccess) return cuda_fail(e, "render kernel launch");
         g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (k > 0) HJ_CUDA(cudaEventRecord(p->ev[k], st));
     }
+    for (size_t k = 1; k < ng; ++k) HJ_CUDA(cudaStreamWaitEvent(stream, p->ev[k], 0));
     return HJ_OK;
 }
 

@@ -372,16 +372,46 @@ __device__ __forceinline__ void colour4(uint32_t yw, int cb0, int cr0, int cb1, 
     w2 = pack4(p2.b, p3.r, p3.g, p3.b);
 }
 
+// 48 RGB bytes (16 pixels) at dst.  Rows of an image whose width is not a
+// multiple of 4 start at any byte offset, so a full item is written as its
+// 11 interior aligned words (funnel-shifted into place) plus the partial
+// words at both ends; only items cropped by the right edge take the
+// byte-wise path.
 __device__ __forceinline__ void store48(uint8_t *__restrict__ dst, const uint32_t (&w)[12], int npx) {
-    if (npx == 16 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
+    if (npx == 16 && (a & 15) == 0) {
         uint4 *d = reinterpret_cast<uint4 *>(dst);
         d[0] = make_uint4(w[0], w[1], w[2], w[3]);
         d[1] = make_uint4(w[4], w[5], w[6], w[7]);
         d[2] = make_uint4(w[8], w[9], w[10], w[11]);
-    } else if (npx == 16 && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+    } else if (npx == 16 && (a & 7) == 0) {
+        uint2 *d = reinterpret_cast<uint2 *>(dst);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) d[i] = make_uint2(w[2 * i], w[2 * i + 1]);
+    } else if (npx == 16 && (a & 3) == 0) {
         uint32_t *d = reinterpret_cast<uint32_t *>(dst);
 #pragma unroll
         for (int i = 0; i < 12; ++i) d[i] = w[i];
+    } else if (npx == 16) {
+        const int m = (int)(a & 3);  // 1..3
+        uint32_t *d = reinterpret_cast<uint32_t *>(dst - m);
+        const unsigned sh = 8u * (unsigned)m;
+        // word k of the aligned span = bytes of w[k-1] (high part) | w[k] (low part)
+#pragma unroll
+        for (int k = 1; k < 12; ++k) d[k] = __funnelshift_l(w[k - 1], w[k], sh);
+        // head: the first 4-m bytes of w[0]; tail: the last m bytes of w[11]
+        if (m == 2) {
+            *reinterpret_cast<uint16_t *>(dst) = (uint16_t)w[0];
+            *reinterpret_cast<uint16_t *>(dst + 46) = (uint16_t)(w[11] >> 16);
+        } else if (m == 1) {
+            dst[0] = (uint8_t)w[0];
+            *reinterpret_cast<uint16_t *>(dst + 1) = (uint16_t)(w[0] >> 8);
+            dst[47] = (uint8_t)(w[11] >> 24);
+        } else {
+            dst[0] = (uint8_t)w[0];
+            *reinterpret_cast<uint16_t *>(dst + 45) = (uint16_t)(w[11] >> 8);
+            dst[47] = (uint8_t)(w[11] >> 24);
+        }
     } else {
         store_partial(dst, make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]),
                       make_uint4(w[8], w[9], w[10], w[11]), npx * 3);
