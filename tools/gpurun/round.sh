@@ -17,7 +17,7 @@ cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
 timeout 200 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err; echo ref rc=$?
 cat gpurun_out/bench_ref.json
 : > gpurun_out/bench_other.json
-for w in 512p420 4096p444 4096p422 24mp420; do
+for w in 512p420 4096p444 4096p422 24mp420 mixed; do
   timeout 200 python bench.py --workload $w --steps 300 --no-cpu-baseline --e2e-steps 3 >> gpurun_out/bench_other.json 2>>gpurun_out/bench.err
 done
 cut -c1-400 gpurun_out/bench_other.json
