@@ -64,6 +64,7 @@ def parse_args():
     ap.add_argument("--batch", type=int, default=0, help="images per GPU per step (0 = default)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = auto")
     ap.add_argument("--e2e-chunk", type=int, default=4, help="images per pipelined H2D/render/D2H chunk")
+    ap.add_argument("--e2e-threads", type=int, default=4, help="host threads calling the render_rows plugin")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", default="images", choices=["images", "rows"],
                     help="N>1: images = each rank its own batch (weak scaling); rows = every rank "
@@ -407,7 +408,8 @@ def run_mixed(args, world, rank, local, pg):
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None},
             "e2e": {"value": round(px_all * e2e_steps / e2e_s / 1e6, 1), "unit": "Mpix/s",
                     "h2d_bytes_per_step": io["h2d_bytes"], "d2h_bytes_per_step": io["d2h_bytes"],
-                    "steps": e2e_steps, "bit_exact_vs_oracle": exact},
+                    "steps": e2e_steps, "bit_exact_vs_oracle": exact,
+                    "api": "pipeline.GpuLane (pinned H2D -> render -> D2H, 3 event-joined streams)"},
             "gpu_launches": int(launches), "clocks": clk,
             "idct_screen": {"exact_fp64_blocks_per_step": round(exact_blocks / args.steps, 1)},
         }
@@ -545,8 +547,32 @@ def main():
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         io = e2e_step()
-    e2e_s = allreduce_max(pg, time.perf_counter() - t0)
+    e2e_lane_s = allreduce_max(pg, time.perf_counter() - t0)
+
+    # ---- e2e through the reference-facing plugin: kernels.cuda.render_rows_*
+    # (the backend contract, kernels/_native.pyx:532-549) called per image from
+    # a pool of host threads, as the reference's lanes call it; host buffers,
+    # each call synchronous H2D -> kernel -> D2H on its thread's stream
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_1311_5304_b200.kernels import cuda as plugin
+    fn = {"444": plugin.render_rows_444, "422": plugin.render_rows_422, "420": plugin.render_rows_420}[sub]
+    mpr = g0.mcus_per_row
+
+    def one(i):
+        c = coeffs[i]
+        fn(c.y_blocks, c.cb_blocks, c.cr_blocks, qts[i], out_arrays[i], w, h, mpr, row0, n_rows)
+
+    n_thr = args.e2e_threads
+    with ThreadPoolExecutor(n_thr) as ex:
+        for _ in range(2):
+            list(ex.map(one, range(batch)))
+        barrier(pg)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            list(ex.map(one, range(batch)))
+        e2e_s = allreduce_max(pg, time.perf_counter() - t0)
     e2e_value = px_all * e2e_steps / e2e_s / 1e6
+    e2e_lane_value = px_all * e2e_steps / e2e_lane_s / 1e6
     # the e2e output must be the kernel's output: spot-check one image against the oracle
     from oracle import oracle
     _, _, c0, q0 = images[0]
@@ -585,7 +611,10 @@ def main():
                          "kernel_ms": round(kernel_ms, 5)},
             "e2e": {"value": round(e2e_value, 1), "unit": "Mpix/s",
                     "h2d_bytes_per_step": io["h2d_bytes"], "d2h_bytes_per_step": io["d2h_bytes"],
-                    "steps": e2e_steps, "bit_exact_vs_oracle": exact},
+                    "steps": e2e_steps, "bit_exact_vs_oracle": exact,
+                    "api": f"kernels.cuda.render_rows_{sub} (reference backend contract) per image from "
+                           f"{n_thr} host threads, pinned host buffers",
+                    "pipelined_lane_mpix_s": round(e2e_lane_value, 1)},
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "amdahl": amdahl,
