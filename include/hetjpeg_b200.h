@@ -189,7 +189,8 @@ hj_status hj_decode_mcu_rows(const uint8_t *data, int64_t n_bytes, int64_t *stat
  * coefficients as hj_decode_mcu_rows, 64-bit bit buffer + 10-bit lookahead
  * with fused run/size/value AC decode, and the scan split at its RSTn markers
  * across up to n_threads host threads (exact: RSTn resets the predictors,
- * kernels/_native.pyx:238-257).  Planes must be zero-initialised.
+ * kernels/_native.pyx:238-257).  Every block of the planes is written (no
+ * pre-zeroing needed).
  * hj_huff_build packs the tables once per scan header. */
 hj_status hj_huff_build(const hj_scan_tables_t *scan, void **fast);
 void hj_huff_free(void *fast);

@@ -26,7 +26,7 @@
 namespace {
 
 const int kZigzag[64] = HJ_ZIGZAG_INIT;
-constexpr int kLook = 10;
+constexpr int kLook = 9;
 
 // AC fast entry: bits 0-15 value (int16), 16-19 run, 20-24 consumed length,
 // 25-27 kind.
@@ -88,6 +88,23 @@ struct Reader {
     int nbits = 0;
 
     inline void refill() {
+        // fast path: the next whole bytes that fit contain no 0xFF (no
+        // stuffing, no marker): append them with one big-endian 64-bit load
+        if (nbits <= 56 && end - p >= 8) {
+            uint64_t w;
+            std::memcpy(&w, p, 8);
+            w = __builtin_bswap64(w);
+            const int nb = (64 - nbits) >> 3;          // 1..8 whole bytes fit
+            const uint64_t top = nb == 8 ? ~0ull : ~(~0ull >> (8 * nb));
+            const uint64_t x = ~w & top;               // a 0xFF byte -> a zero byte of x
+            const uint64_t has_ff = (x - 0x0101010101010101ull) & ~x & 0x8080808080808080ull & top;
+            if (!has_ff) {
+                acc |= (w & top) >> nbits;
+                p += nb;
+                nbits += 8 * nb;
+                return;
+            }
+        }
         while (nbits <= 56) {
             if (p >= end) return;
             uint8_t b = *p;
@@ -147,6 +164,7 @@ inline int decode_sym(Reader &br, const Table &t, int &err) {
 }
 
 inline int decode_block(Reader &br, const Table &dc, const Table &ac, int16_t *out, int64_t &pred) {
+    std::memset(out, 0, 64 * sizeof(int16_t));  // the block is about to be hot anyway
     int err = HJ_OK;
     int t = decode_sym(br, dc, err);
     if (err) return err;
@@ -253,7 +271,8 @@ hj_status hj_huff_build(const hj_scan_tables_t *scan, void **out) {
 
 void hj_huff_free(void *fast) { delete static_cast<Fast *>(fast); }
 
-// Decode a whole scan (all MCUs) into zero-initialised planes.  With a
+// Decode a whole scan (all MCUs) into the planes (every block is written,
+// zeros included).  With a
 // restart interval the intervals are decoded on up to n_threads threads.
 hj_status hj_decode_scan_fast(const void *fast, const uint8_t *data, int64_t n, int16_t *y, int16_t *cb,
                               int16_t *cr, int32_t mcus_per_row, int32_t mcu_rows, int32_t y_per_mcu,

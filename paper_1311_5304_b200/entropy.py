@@ -185,10 +185,6 @@ class FastScan:
         buf = np.frombuffer(data, dtype=np.uint8)[sp.offset:sp.offset + sp.length]
         if out is None:
             out = alloc_coefficients(self.geometry, pinned=pinned)
-        else:
-            out.y_blocks[...] = 0
-            out.cb_blocks[...] = 0
-            out.cr_blocks[...] = 0
         g = self.geometry
         st = _lib.lib.hj_decode_scan_fast(self._h, buf.ctypes.data, len(buf), out.y_blocks.ctypes.data,
                                           out.cb_blocks.ctypes.data, out.cr_blocks.ctypes.data,
