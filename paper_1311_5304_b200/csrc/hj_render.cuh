@@ -23,7 +23,9 @@ static_assert(sizeof(Tile) == 32, "Tile layout");
 // CTA size and residency: small CTAs sweep their strips independently, so
 // barrier waits stay local to a strip.  4:2:0 uses 4-warp CTAs (its wider
 // per-step pixel work balances the float64 fallback better), 4:4:4 / 4:2:2
-// 2-warp CTAs; 168 registers per thread, no spills.
+// 2-warp CTAs.  CTAs per SM (launch bounds): 4:4:4 has the smallest planes,
+// so it runs 8 CTAs (16 warps, 128 registers); 4:2:2 / 4:2:0 are limited by
+// shared memory to 12 warps (168 registers).  Measured: tools/experiments.
 #ifndef HJ_THREADS_420
 #define HJ_THREADS_420 128
 #endif
@@ -31,7 +33,18 @@ static_assert(sizeof(Tile) == 32, "Tile layout");
 #define HJ_THREADS 64
 #endif
 constexpr int threads_for(int sub) { return sub == HJ_SUB_420 ? HJ_THREADS_420 : HJ_THREADS; }
-constexpr int ctas_per_sm(int sub) { return 384 / threads_for(sub); }
+#ifndef HJ_CTAS_444
+#define HJ_CTAS_444 8
+#endif
+#ifndef HJ_CTAS_422
+#define HJ_CTAS_422 6
+#endif
+#ifndef HJ_CTAS_420
+#define HJ_CTAS_420 3
+#endif
+constexpr int ctas_per_sm(int sub) {
+    return sub == HJ_SUB_444 ? HJ_CTAS_444 : sub == HJ_SUB_422 ? HJ_CTAS_422 : HJ_CTAS_420;
+}
 // Strip widths (MCUs per CTA) so one sweep step has ~threads two-block jobs:
 // 444 -> ceil(S/2) + S, 422 -> S + (S+2), 420 -> 2S + (S+2).
 constexpr int strip_for(int sub) {
