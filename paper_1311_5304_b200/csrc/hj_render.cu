@@ -251,10 +251,11 @@ __device__ __noinline__ uint2 exact_block_x8(const int16_t *__restrict__ src, co
 // ------------------------------------------------------------- geometry
 
 // Chroma planes: 4:4:4 keeps Cb and Cr as byte planes (no filter).  4:2:2 /
-// 4:2:0 keep SWAR words (c_cb | c_cr << 16) << CSH so the fancy filters run
-// on both planes per 32-bit op; 4:2:0 scales by 16 and 4:2:2 by 64 so the
-// filtered values land in byte 1 / byte 3 of each word (every lane stays
-// below 2^16).  The 4:2:x chroma window covers MCUs [m0-1, m1+1).
+// 4:2:0 store one (Cb | Cr << 8) pair per position and widen it on read to
+// SWAR words (c_cb | c_cr << 16) << CSH, so the fancy filters run on both
+// planes per 32-bit op; 4:2:0 scales by 16 and 4:2:2 by 64 so the filtered
+// values land in byte 1 / byte 3 of each word (every lane stays below 2^16).
+// The 4:2:x chroma window covers MCUs [m0-1, m1+1).
 template <int SUB>
 struct Geo;
 template <>
@@ -296,7 +297,9 @@ struct Smem {
     // 4:4:4: Cb, Cr byte planes (two slots); 4:2:x: SWAR chroma rows
     alignas(16) uint8_t cbp[SUB == HJ_SUB_444 ? 2 : 1][SUB == HJ_SUB_444 ? 8 * G::YW : 16];
     alignas(16) uint8_t crp[SUB == HJ_SUB_444 ? 2 : 1][SUB == HJ_SUB_444 ? 8 * G::YW : 16];
-    alignas(16) uint32_t cs[SUB == HJ_SUB_444 ? 1 : G::CROWS][SUB == HJ_SUB_444 ? 4 : G::CW];
+    // 4:2:x chroma: one 16-bit (Cb | Cr << 8) pair per sample position; the
+    // pixel stage widens it to SWAR words (2 bytes/position keeps 16 warps/SM)
+    alignas(16) uint16_t cs[SUB == HJ_SUB_444 ? 1 : G::CROWS][SUB == HJ_SUB_444 ? 8 : G::CW];
     alignas(16) float qf[3][64];            // binary32 q * pre (screen)
     int qi[3][64];                          // integer q (exact path)
     double g[kExactGroups<SUB>][64];        // exact-path column results
@@ -314,20 +317,14 @@ __device__ __forceinline__ void write_block_rows(uint8_t *dst, int stride, const
     for (int r = 0; r < 8; ++r) *reinterpret_cast<uint2 *>(dst + r * stride) = make_uint2(a[2 * r], a[2 * r + 1]);
 }
 
-// SWAR chroma rows: word k = (cb_k | cr_k << 16) << CSH, 8 words per row.
-template <int CSH>
-__device__ __forceinline__ void write_swar_rows(uint32_t *cs, int stride, const uint32_t (&cb)[16],
-                                                const uint32_t (&cr)[16]) {
+// Chroma rows: position k = cb_k | cr_k << 8, 8 positions (16 bytes) per row.
+__device__ __forceinline__ void write_c16_rows(uint16_t *cs, int stride, const uint32_t (&cb)[16],
+                                               const uint32_t (&cr)[16]) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t a = cb[2 * r + h], b = cr[2 * r + h];
-            const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
-            sts128(cs + r * stride + 4 * h,
-                   make_uint4(__byte_perm(t0, 0, 0x4140) << CSH, __byte_perm(t0, 0, 0x4342) << CSH,
-                              __byte_perm(t1, 0, 0x4140) << CSH, __byte_perm(t1, 0, 0x4342) << CSH));
-        }
+        const uint32_t a0 = cb[2 * r], a1 = cb[2 * r + 1], b0 = cr[2 * r], b1 = cr[2 * r + 1];
+        sts128(cs + r * stride, make_uint4(__byte_perm(a0, b0, 0x5140), __byte_perm(a0, b0, 0x7362),
+                                           __byte_perm(a1, b1, 0x5140), __byte_perm(a1, b1, 0x7362)));
     }
 }
 
@@ -508,14 +505,18 @@ __device__ __forceinline__ void render16_444(uint8_t *__restrict__ dst, uint4 yv
     store48(dst, w, npx);
 }
 
-// 10 SWAR words of one chroma row: p[-1], p[0..7], p[8] with edge
-// replication at the padded plane's first / last column.
-__device__ __forceinline__ void load_c10(const uint32_t *p, bool left_edge, bool right_edge, uint32_t (&c)[10]) {
-    const uint4 m0 = lds128(p), m1 = lds128(p + 4);
-    c[1] = m0.x; c[2] = m0.y; c[3] = m0.z; c[4] = m0.w;
-    c[5] = m1.x; c[6] = m1.y; c[7] = m1.z; c[8] = m1.w;
-    c[0] = left_edge ? c[1] : p[-1];
-    c[9] = right_edge ? c[8] : p[8];
+// 10 SWAR words (cb | cr << 16) of one chroma row from the 16-bit pair
+// storage: positions p[-1], p[0..7], p[8], with edge replication at the
+// padded plane's first / last column.
+__device__ __forceinline__ uint32_t widen(uint32_t pair) { return __byte_perm(pair, 0, 0x4140); }
+__device__ __forceinline__ void load_c10(const uint16_t *p, bool left_edge, bool right_edge, uint32_t (&c)[10]) {
+    const uint4 m = lds128(p);
+    c[1] = __byte_perm(m.x, 0, 0x4140); c[2] = __byte_perm(m.x, 0, 0x4342);
+    c[3] = __byte_perm(m.y, 0, 0x4140); c[4] = __byte_perm(m.y, 0, 0x4342);
+    c[5] = __byte_perm(m.z, 0, 0x4140); c[6] = __byte_perm(m.z, 0, 0x4342);
+    c[7] = __byte_perm(m.w, 0, 0x4140); c[8] = __byte_perm(m.w, 0, 0x4342);
+    c[0] = left_edge ? c[1] : widen(p[-1]);
+    c[9] = right_edge ? c[8] : widen(p[8]);
 }
 
 template <int SUB>
@@ -596,7 +597,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                 bool has_b = true;
                 uint32_t dA, dB;                   // exact-path destinations
                 uint8_t *ydst = nullptr;           // Y-like byte rows
-                uint32_t *cdst = nullptr;          // SWAR rows
+                uint16_t *cdst = nullptr;          // chroma pair rows
                 int cw0 = 0;
                 if (is_y) {
                     int64_t yblk;
@@ -634,10 +635,8 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                         if constexpr (SUB == HJ_SUB_420) {
                             // the slot's old row 7 (MCU row crow-3) is the top
                             // context of MCU row crow-2, drawn this step
-                            uint32_t *save = &sm.cs[24][0] + 8 * lm;
-                            const uint32_t *old = cdst + 7 * G::CW;
-                            sts128(save, lds128(old));
-                            sts128(save + 4, lds128(old + 4));
+                            uint16_t *save = &sm.cs[24][0] + 8 * lm;
+                            sts128(save, lds128(cdst + 7 * G::CW));
                         }
                     }
                 }
@@ -666,7 +665,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                         for (int i = 0; i < 16; ++i) keep[i] = w[i];
                         okA = ok;
                     } else {
-                        if (!direct) write_swar_rows<G::CSH>(cdst, G::CW, keep, w);
+                        if (!direct) write_c16_rows(cdst, G::CW, keep, w);
                         const uint32_t blk = (uint32_t)((int64_t)crow * mpr + m);
                         if (!okA) push_exact(nq, queue, qdst, (1u << 30) | blk, dA);
                         if (!ok) push_exact(nq, queue, qdst, (2u << 30) | blk, dB);
@@ -692,10 +691,10 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                 if (kind == 0) {
                     *reinterpret_cast<uint2 *>(smem_raw + off + l * G::YW) = row;
                 } else if constexpr (SUB != HJ_SUB_444) {
-                    uint16_t *c16 = reinterpret_cast<uint16_t *>(&sm.cs[0][0] + off + l * G::CW) + (kind & 1);
+                    uint8_t *c8 = reinterpret_cast<uint8_t *>(&sm.cs[0][0] + off + l * G::CW) + (kind & 1);
 #pragma unroll
                     for (int c = 0; c < 8; ++c)
-                        c16[2 * c] = (uint16_t)(((c < 4 ? row.x >> (8 * c) : row.y >> (8 * (c - 4))) & 0xff) << G::CSH);
+                        c8[2 * c] = (uint8_t)(c < 4 ? row.x >> (8 * c) : row.y >> (8 * (c - 4)));
                 }
             }
             if (tid == 0 && n) atomicAdd(&g_exact_blocks, (unsigned long long)n);
@@ -713,12 +712,12 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                 const int n_items = 8 * S;
                 const int gw = S;
                 const float inv_w = 1.0f / (float)gw;
-                const uint32_t *cnear = &sm.cs[0][0] + (R % 3) * 8 * G::CW;
-                const uint32_t *cnext = &sm.cs[0][0] + ((R + 1) % 3) * 8 * G::CW;
+                const uint16_t *cnear = &sm.cs[0][0] + (R % 3) * 8 * G::CW;
+                const uint16_t *cnext = &sm.cs[0][0] + ((R + 1) % 3) * 8 * G::CW;
                 // top context of the MCU row's first sample row: the last row
                 // of MCU row R-1 - saved in row 24 when this step's chroma
                 // jobs overwrote its slot, else still in the slot
-                const uint32_t *cprev = do_c ? &sm.cs[24][0] : &sm.cs[0][0] + (((R + 2) % 3) * 8 + 7) * G::CW;
+                const uint16_t *cprev = do_c ? &sm.cs[24][0] : &sm.cs[0][0] + (((R + 2) % 3) * 8 + 7) * G::CW;
 #pragma unroll 1
                 for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
                     const int i = i0;
@@ -731,22 +730,22 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     const int npx = min(16, im.width - x0);
                     if (npx <= 0) continue;
                     const int kw = 8 * (g + 1);  // window word of the MCU's chroma column 0
-                    const uint32_t *pn = cnear + p * G::CW + kw;
-                    const uint32_t *pu = p > 0 ? pn - G::CW : (R > 0 ? cprev + kw : pn);
-                    const uint32_t *pd = p < 7 ? pn + G::CW : (R + 1 < mcu_rows ? cnext + kw : pn);
+                    const uint16_t *pn = cnear + p * G::CW + kw;
+                    const uint16_t *pu = p > 0 ? pn - G::CW : (R > 0 ? cprev + kw : pn);
+                    const uint16_t *pd = p < 7 ? pn + G::CW : (R + 1 < mcu_rows ? cnext + kw : pn);
                     const bool le = left_edge && g == 0, re = right_edge && g == S - 1;
                     // colsum = 3*near + far per lane (libjpeg h2v2 fancy), 16x scaled
                     uint32_t n3[10];
                     load_c10(pn, le, re, n3);
 #pragma unroll
-                    for (int k = 0; k < 10; ++k) n3[k] *= 3u;
+                    for (int k = 0; k < 10; ++k) n3[k] *= 48u;
                     const int rows = min(2, im.height - y0);
 #pragma unroll 1
                     for (int h = 0; h < rows; ++h) {
                         uint32_t cs10[10];
                         load_c10(h ? pd : pu, le, re, cs10);
 #pragma unroll
-                        for (int k = 0; k < 10; ++k) cs10[k] += n3[k];
+                        for (int k = 0; k < 10; ++k) cs10[k] = cs10[k] * 16u + n3[k];
                         // even 16(3cs+prev+8), odd 16(3cs+next+7)
                         render16_swar(im.rgb + ((int64_t)(y0 + h) * im.width + x0) * 3,
                                       lds128(yp + (2 * p + h) * G::YW + 16 * g), cs10, 0x00800080u, 0x00700070u,
@@ -758,7 +757,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                 const int n_items = 8 * S;
                 const int gw = S;
                 const float inv_w = 1.0f / (float)gw;
-                const uint32_t *crow0 = &sm.cs[0][0] + (par ^ 1) * 8 * G::CW;
+                const uint16_t *crow0 = &sm.cs[0][0] + (par ^ 1) * 8 * G::CW;
 #pragma unroll 1
                 for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
                     const int i = i0;
@@ -771,6 +770,8 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     if (npx <= 0) continue;
                     uint32_t c10[10];
                     load_c10(crow0 + y * G::CW + 8 * (g + 1), left_edge && g == 0, right_edge && g == S - 1, c10);
+#pragma unroll
+                    for (int k = 0; k < 10; ++k) c10[k] <<= 6;
                     // h2v1 on 64x-scaled lanes: even 64(3c+prev+1), odd 64(3c+next+2)
                     render16_swar(im.rgb + ((int64_t)yy * im.width + x0) * 3, lds128(yp + y * G::YW + 16 * g),
                                   c10, 0x00400040u, 0x00800080u, npx);

@@ -23,9 +23,10 @@ static_assert(sizeof(Tile) == 32, "Tile layout");
 // CTA size and residency: small CTAs sweep their strips independently, so
 // barrier waits stay local to a strip.  4:2:0 uses 4-warp CTAs (its wider
 // per-step pixel work balances the float64 fallback better), 4:4:4 / 4:2:2
-// 2-warp CTAs.  CTAs per SM (launch bounds): 4:4:4 has the smallest planes,
-// so it runs 8 CTAs (16 warps, 128 registers); 4:2:2 / 4:2:0 are limited by
-// shared memory to 12 warps (168 registers).  Measured: tools/experiments.
+// 2-warp CTAs.  CTAs per SM (launch bounds): 4:4:4 runs 8 CTAs and 4:2:0 4
+// CTAs (16 warps, 128 registers; 4:2:x chroma is stored as 2-byte pairs to
+// fit), 4:2:2 6 CTAs (12 warps, 168 registers: it was slower at 16).
+// Measured: tools/experiments/README.md.
 #ifndef HJ_THREADS_420
 #define HJ_THREADS_420 128
 #endif
@@ -40,7 +41,7 @@ constexpr int threads_for(int sub) { return sub == HJ_SUB_420 ? HJ_THREADS_420 :
 #define HJ_CTAS_422 6
 #endif
 #ifndef HJ_CTAS_420
-#define HJ_CTAS_420 3
+#define HJ_CTAS_420 4
 #endif
 constexpr int ctas_per_sm(int sub) {
     return sub == HJ_SUB_444 ? HJ_CTAS_444 : sub == HJ_SUB_422 ? HJ_CTAS_422 : HJ_CTAS_420;
