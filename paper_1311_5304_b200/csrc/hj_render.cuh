@@ -30,10 +30,15 @@ static_assert(sizeof(Tile) == 32, "Tile layout");
 #ifndef HJ_THREADS_420
 #define HJ_THREADS_420 128
 #endif
+#ifndef HJ_THREADS_422
+#define HJ_THREADS_422 64
+#endif
 #ifndef HJ_THREADS
 #define HJ_THREADS 64
 #endif
-constexpr int threads_for(int sub) { return sub == HJ_SUB_420 ? HJ_THREADS_420 : HJ_THREADS; }
+constexpr int threads_for(int sub) {
+    return sub == HJ_SUB_420 ? HJ_THREADS_420 : sub == HJ_SUB_422 ? HJ_THREADS_422 : HJ_THREADS;
+}
 #ifndef HJ_CTAS_444
 #define HJ_CTAS_444 8
 #endif
