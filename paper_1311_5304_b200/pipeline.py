@@ -82,11 +82,11 @@ class BatchDecoder:
     """End-to-end batch decode: host Huffman on a thread pool (native C++,
     GIL released) pipelined with the B200 parallel phase.
 
-    As each image's entropy decode finishes (into page-locked coefficient
-    buffers) the orchestrating thread queues H2D -> render -> D2H for it on
-    the next of `n_streams` CUDA streams, so the GPU work of finished images
-    overlaps the Huffman decoding of the rest - the paper's pipelined scheme
-    (§5.3) at batch granularity.  `huffman_only()` times the same
+    Each host worker entropy-decodes an image (into page-locked coefficient
+    buffers) and then queues that image's H2D -> render -> D2H on its own
+    CUDA stream, so the GPU work of finished images overlaps the Huffman
+    decoding of the rest with no central dispatcher in the way - the paper's
+    pipelined scheme (§5.3) at batch granularity.  `huffman_only()` times the same
     host stage alone (same decoder, same thread count): T_huff of the Amdahl
     bound wall / huffman (orchestrator.py:71-75).
     """
@@ -106,9 +106,12 @@ class BatchDecoder:
         self.coeffs = [entropy.alloc_coefficients(g, pinned=True) for g in self.geos]
         self.pixels = [alloc_pixels(g.width, g.height, pinned=True) for g in self.geos]
         self.batch = device.DeviceBatch(self.geos, fast=fast)
-        self.streams = [device.Stream() for _ in range(max(1, n_streams))]
+        # one CUDA stream per host worker: a worker that finishes an image's
+        # entropy decode queues that image's H2D -> render -> D2H itself
+        self.streams = [device.Stream() for _ in range(max(1, n_streams, self.threads))]
         for i in range(len(self.geos)):
             self.batch.upload_qtables(i, self.q[i], self.streams[0])
+            self.batch.render_items([(i, 0, self.geos[i].mcu_rows)], self.streams[0])  # cache the plans
         self.streams[0].synchronize()
 
     def _huff(self, i: int) -> int:
@@ -126,22 +129,31 @@ class BatchDecoder:
 
     def run(self) -> dict:
         """Decode the whole batch into self.pixels; returns wall seconds and bytes moved."""
+        import threading
         import time
-        from concurrent.futures import ThreadPoolExecutor, as_completed
+        from concurrent.futures import ThreadPoolExecutor
         b = self.batch
-        h2d = d2h = 0
+        slot = threading.local()
+        counter = iter(range(len(self.streams)))
+        lock = threading.Lock()
+
+        def work(i):
+            if not hasattr(slot, "stream"):
+                with lock:
+                    slot.stream = self.streams[next(counter)]
+            self._huff(i)
+            s = slot.stream
+            h2d = b.upload_coefficients(i, self.coeffs[i], s)
+            b.render_items([(i, 0, self.geos[i].mcu_rows)], s)
+            return h2d, b.download_rgb(i, self.pixels[i].data, s)
+
         t0 = time.perf_counter()
         with ThreadPoolExecutor(self.threads) as ex:
-            futs = [ex.submit(self._huff, i) for i in range(len(self.blobs))]
-            for k, f in enumerate(as_completed(futs)):
-                i = f.result()
-                s = self.streams[k % len(self.streams)]
-                h2d += b.upload_coefficients(i, self.coeffs[i], s)
-                b.render_items([(i, 0, self.geos[i].mcu_rows)], s)
-                d2h += b.download_rgb(i, self.pixels[i].data, s)
+            moved = list(ex.map(work, range(len(self.blobs))))
         for s in self.streams:
             s.synchronize()
-        return {"wall_s": time.perf_counter() - t0, "h2d_bytes": h2d, "d2h_bytes": d2h}
+        return {"wall_s": time.perf_counter() - t0, "h2d_bytes": sum(m[0] for m in moved),
+                "d2h_bytes": sum(m[1] for m in moved)}
 
     def close(self):
         self.batch.close()
