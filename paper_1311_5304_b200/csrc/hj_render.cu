@@ -738,14 +738,14 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     uint32_t n3[10];
                     load_c10(pn, le, re, n3);
 #pragma unroll
-                    for (int k = 0; k < 10; ++k) n3[k] *= 48u;
+                    for (int k = 0; k < 10; ++k) n3[k] *= 3u << G::CSH;
                     const int rows = min(2, im.height - y0);
 #pragma unroll 1
                     for (int h = 0; h < rows; ++h) {
                         uint32_t cs10[10];
                         load_c10(h ? pd : pu, le, re, cs10);
 #pragma unroll
-                        for (int k = 0; k < 10; ++k) cs10[k] = cs10[k] * 16u + n3[k];
+                        for (int k = 0; k < 10; ++k) cs10[k] = (cs10[k] << G::CSH) + n3[k];
                         // even 16(3cs+prev+8), odd 16(3cs+next+7)
                         render16_swar(im.rgb + ((int64_t)(y0 + h) * im.width + x0) * 3,
                                       lds128(yp + (2 * p + h) * G::YW + 16 * g), cs10, 0x00800080u, 0x00700070u,
@@ -771,7 +771,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     uint32_t c10[10];
                     load_c10(crow0 + y * G::CW + 8 * (g + 1), left_edge && g == 0, right_edge && g == S - 1, c10);
 #pragma unroll
-                    for (int k = 0; k < 10; ++k) c10[k] <<= 6;
+                    for (int k = 0; k < 10; ++k) c10[k] <<= G::CSH;
                     // h2v1 on 64x-scaled lanes: even 64(3c+prev+1), odd 64(3c+next+2)
                     render16_swar(im.rgb + ((int64_t)yy * im.width + x0) * 3, lds128(yp + y * G::YW + 16 * g),
                                   c10, 0x00400040u, 0x00800080u, npx);
