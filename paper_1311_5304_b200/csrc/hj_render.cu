@@ -260,7 +260,7 @@ template <int SUB>
 struct Geo;
 template <>
 struct Geo<HJ_SUB_444> {
-    static constexpr int S = kStrip444, MW = 8, MH = 8, CSH = 0;
+    static constexpr int S = kStrip444, MW = 8, MH = 8;
     static constexpr int YW = 8 * S;      // Y / Cb / Cr plane width (bytes)
     static constexpr int CW = 0;
     static constexpr int YSLOTS = 2;
