@@ -1,7 +1,6 @@
 """Host-side logic on the CPU: the C ABI exports, the parser (incl. the 4:2:0
 extension), and the native C++ Huffman decoder against the reference's own
 coefficients (golden fixtures).  No GPU calls."""
-import ctypes
 import os
 import re
 

@@ -3,8 +3,6 @@ their timings with a max (the bench's only collective)."""
 import os
 import socket
 
-import pytest
-
 from paper_1311_5304_b200 import shard
 
 
