@@ -108,6 +108,26 @@ __device__ __forceinline__ Rgb colour(int y, int cb, int cr, bool &special) {
     return Rgb{y + (rs >> kColK), y + (gs >> kColK), y + (bs >> kColK)};
 }
 
+// The additive colour constants held in registers: the multiplier goes into
+// IMAD's immediate slot and the constant stays in a register instead of
+// being rematerialised per pixel (IMAD takes one immediate).  The empty asm
+// hides the values from constant folding.
+struct ColourRegs {
+    int cr, cb, cg, ar, ab, agb, agr;
+};
+__device__ __forceinline__ ColourRegs colour_regs() {
+    ColourRegs k{HJ_COL_CR, HJ_COL_CB, HJ_COL_CG, HJ_COL_AR, HJ_COL_AB, HJ_COL_AGB, HJ_COL_AGR};
+    asm("" : "+r"(k.cr), "+r"(k.cb), "+r"(k.cg), "+r"(k.ar), "+r"(k.ab), "+r"(k.agb), "+r"(k.agr));
+    return k;
+}
+__device__ __forceinline__ Rgb colour(int y, int cb, int cr, bool &special, const ColourRegs &k) {
+    int rs = k.ar * cr + k.cr;
+    int bs = k.ab * cb + k.cb;
+    int gs = k.agb * cb + (k.agr * cr + k.cg);
+    special |= (gs == kGSpecial);
+    return Rgb{y + (rs >> kColK), y + (gs >> kColK), y + (bs >> kColK)};
+}
+
 // The tie-pair correction for one pixel (rarely executed).
 __device__ __forceinline__ int colour_g_exact(int y, int cb, int cr) {
     int g = y + ((HJ_COL_AGB * cb + HJ_COL_AGR * cr + HJ_COL_CG) >> kColK);

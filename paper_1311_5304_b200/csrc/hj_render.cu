@@ -359,11 +359,11 @@ __device__ __forceinline__ int grab32(int *taken) {
 // registers instead of being rematerialised per pixel.
 __device__ __forceinline__ void colour4(uint32_t yw, int cb0, int cr0, int cb1, int cr1, int cb2, int cr2,
                                         int cb3, int cr3, bool &special, uint32_t &w0, uint32_t &w1,
-                                        uint32_t &w2) {
-    const Rgb p0 = colour((int)__byte_perm(yw, 0, 0x4440), cb0, cr0, special);
-    const Rgb p1 = colour((int)__byte_perm(yw, 0, 0x4441), cb1, cr1, special);
-    const Rgb p2 = colour((int)__byte_perm(yw, 0, 0x4442), cb2, cr2, special);
-    const Rgb p3 = colour((int)__byte_perm(yw, 0, 0x4443), cb3, cr3, special);
+                                        uint32_t &w2, const ColourRegs &k) {
+    const Rgb p0 = colour((int)__byte_perm(yw, 0, 0x4440), cb0, cr0, special, k);
+    const Rgb p1 = colour((int)__byte_perm(yw, 0, 0x4441), cb1, cr1, special, k);
+    const Rgb p2 = colour((int)__byte_perm(yw, 0, 0x4442), cb2, cr2, special, k);
+    const Rgb p3 = colour((int)__byte_perm(yw, 0, 0x4443), cb3, cr3, special, k);
     w0 = pack4(p0.r, p0.g, p0.b, p1.r);
     w1 = pack4(p1.g, p1.b, p2.r, p2.g);
     w2 = pack4(p2.b, p3.r, p3.g, p3.b);
@@ -469,6 +469,7 @@ __device__ __forceinline__ void render16_swar(uint8_t *__restrict__ dst, uint4 y
     const uint32_t yw[4] = {yv.x, yv.y, yv.z, yv.w};
     uint32_t w[12];
     bool special = false;
+    const ColourRegs k = colour_regs();
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const uint32_t ta = c[2 * q + 1] * 3u, tb = c[2 * q + 2] * 3u;
@@ -476,7 +477,7 @@ __device__ __forceinline__ void render16_swar(uint8_t *__restrict__ dst, uint4 y
         const uint32_t e1 = tb + c[2 * q + 1] + rnd_e, o1 = tb + c[2 * q + 3] + rnd_o;
         colour4(yw[q], (int)__byte_perm(e0, 0, 0x4441), (int)(e0 >> 24), (int)__byte_perm(o0, 0, 0x4441),
                 (int)(o0 >> 24), (int)__byte_perm(e1, 0, 0x4441), (int)(e1 >> 24),
-                (int)__byte_perm(o1, 0, 0x4441), (int)(o1 >> 24), special, w[3 * q], w[3 * q + 1], w[3 * q + 2]);
+                (int)__byte_perm(o1, 0, 0x4441), (int)(o1 >> 24), special, w[3 * q], w[3 * q + 1], w[3 * q + 2], k);
     }
     if (special) {
         render16_exact(dst, yv, make_uint4(c[0], c[1], c[2], c[3]), make_uint4(c[4], c[5], c[6], c[7]),
@@ -492,12 +493,13 @@ __device__ __forceinline__ void render16_444(uint8_t *__restrict__ dst, uint4 yv
                    rw[4] = {rv.x, rv.y, rv.z, rv.w};
     uint32_t w[12];
     bool special = false;
+    const ColourRegs k = colour_regs();
 #pragma unroll
     for (int q = 0; q < 4; ++q)
         colour4(yw[q], (int)(bw[q] & 0xff), (int)((rw[q]) & 0xff), (int)__byte_perm(bw[q], 0, 0x4441),
                 (int)__byte_perm(rw[q], 0, 0x4441), (int)__byte_perm(bw[q], 0, 0x4442),
                 (int)__byte_perm(rw[q], 0, 0x4442), (int)(bw[q] >> 24), (int)(rw[q] >> 24), special, w[3 * q],
-                w[3 * q + 1], w[3 * q + 2]);
+                w[3 * q + 1], w[3 * q + 2], k);
     if (special) {
         render16_exact(dst, yv, bv, rv, make_uint2(0, 0), 0, 0, 1, npx);
         return;
