@@ -29,6 +29,7 @@
 // Sample planes are double (Y) / triple (4:2:0 chroma) buffered across steps.
 // One thread prefetches the next step's coefficient ranges into L2 with
 // bulk prefetches (cp.async.bulk.prefetch.L2).
+#include <atomic>
 #include <cstdint>
 
 #include "hj_common.cuh"
@@ -806,13 +807,18 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
 
 template <int SUB>
 cudaError_t launch_sub(const hj_image_t *images, const Tile *tiles, int n_tiles, cudaStream_t stream) {
-    static bool configured = false;
+    // the dynamic shared-memory opt-in is per device; set it once per device
+    // (thread-safe: a racing second setter is harmless and idempotent)
+    static std::atomic<uint64_t> configured{0};
     const int bytes = (int)sizeof(Smem<SUB>);
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(render_kernel<SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              bytes);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(configured.load(std::memory_order_acquire) & bit)) {
+        e = cudaFuncSetAttribute(render_kernel<SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         if (e != cudaSuccess) return e;
-        configured = true;
+        configured.fetch_or(bit, std::memory_order_release);
     }
     render_kernel<SUB><<<n_tiles, kNT<SUB>, bytes, stream>>>(images, tiles);
     return cudaGetLastError();
