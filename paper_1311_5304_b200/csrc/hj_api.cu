@@ -16,6 +16,8 @@
 
 #include "hj_render.cuh"
 
+
+
 namespace {
 
 thread_local std::string t_error;
@@ -75,34 +77,63 @@ struct Plan {
     }
 };
 
+// Rows per tile T: every tile pays fill / drain steps (and 4:2:0 tiles
+// re-transform two chroma MCU rows of vertical context), while too few
+// tiles leave resident CTA slots idle in the last wave.  T minimises the
+// modelled makespan  waves(T) * (T + overhead),  waves = ceil(tiles / slots),
+// over T in [4, 96] with at least `min_waves` waves when the batch allows it
+// (several waves even out the float64-fallback variance between tiles;
+// measured: 4:2:0 is best at 2, 4:4:4 / 4:2:2 at 4+).  A batch too small to
+// fill one wave first gets narrower strips.
+int choose_rows_per_tile(const hj_image_t *images, int n, int sub, int direct, int S, int64_t slots) {
+    const double overhead = sub == HJ_SUB_420 ? 1.5 : 0.7;  // in steps
+    const int64_t min_waves = sub == HJ_SUB_420 ? 2 : 4;
+    int best_T = 8;
+    double best = 1e300;
+    for (int T = 4; T <= 96; ++T) {
+        int64_t tiles = 0;
+        for (int i = 0; i < n; ++i) {
+            const hj_image_t &im = images[i];
+            if (im.subsampling != sub || ((im.flags & HJ_FLAG_DIRECT_IDCT) != 0) != (direct != 0)) continue;
+            tiles += (int64_t)((im.mcus_per_row + S - 1) / S) * ((im.n_rows + T - 1) / T);
+        }
+        if (tiles == 0) return best_T;
+        const int64_t waves = (tiles + slots - 1) / slots;
+        if (waves < min_waves && T > 8) continue;  // short tiles only for tiny batches
+        const double cost = (double)waves * (T + overhead);
+        if (cost < best - 1e-9) {
+            best = cost;
+            best_T = T;
+        }
+    }
+    return best_T;
+}
+
 void build_tiles(const hj_image_t *images, int n, std::vector<hj::Tile> &tiles,
                  std::vector<Plan::Group> &groups) {
     int sms = 148;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     for (int sub = HJ_SUB_444; sub <= HJ_SUB_420; ++sub) {
-        const int64_t target = (int64_t)sms * hj::ctas_per_sm(sub) * 6;  // ~6 waves of resident CTAs
+        const int64_t slots = (int64_t)sms * hj::ctas_per_sm(sub);  // resident CTAs
         for (int direct = 0; direct < 2; ++direct) {
-            // rows per tile: enough tiles for ~6 waves, but 4:2:0 tiles re-transform
-            // two chroma MCU rows of vertical context, so keep them >= 8 rows; a
-            // small batch first gets narrower strips (only 2 chroma MCUs of
-            // horizontal context each) before shorter tiles
-            const int t_min = 8;  // a tile pays one fill and one drain step
             int S = hj::strip_width(sub);
-            int64_t strip_rows = 0;
-            int T = t_min;
+            int64_t strip_rows = 0, strips = 0;
             for (;;) {
-                strip_rows = 0;
+                strip_rows = strips = 0;
                 for (int i = 0; i < n; ++i) {
                     const hj_image_t &im = images[i];
                     if (im.subsampling != sub || ((im.flags & HJ_FLAG_DIRECT_IDCT) != 0) != (direct != 0)) continue;
-                    strip_rows += (int64_t)((im.mcus_per_row + S - 1) / S) * im.n_rows;
+                    const int64_t ns = (im.mcus_per_row + S - 1) / S;
+                    strips += ns;
+                    strip_rows += ns * im.n_rows;
                 }
-                T = (int)std::min<int64_t>(64, std::max<int64_t>(t_min, (strip_rows + target - 1) / target));
-                if (strip_rows == 0 || strip_rows / T >= target / 3 || S <= 12) break;
+                // narrower strips only when 8-row tiles could not fill a third of a wave
+                if (strip_rows == 0 || strip_rows / 8 >= slots / 3 || S <= 12) break;
                 S = (S + 1) / 2;
             }
             if (strip_rows == 0) continue;
+            const int T = choose_rows_per_tile(images, n, sub, direct, S, slots);
             Plan::Group g{sub, direct != 0, (int)tiles.size(), 0};
             for (int i = 0; i < n; ++i) {
                 const hj_image_t &im = images[i];
