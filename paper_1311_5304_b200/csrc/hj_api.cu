@@ -16,6 +16,20 @@
 
 #include "hj_render.cuh"
 
+// tile-planner model parameters (choose_rows_per_tile)
+#ifndef HJ_PLAN_OVH_420
+#define HJ_PLAN_OVH_420 1.5
+#endif
+#ifndef HJ_PLAN_OVH
+#define HJ_PLAN_OVH 0.7
+#endif
+#ifndef HJ_PLAN_MINW_420
+#define HJ_PLAN_MINW_420 2
+#endif
+#ifndef HJ_PLAN_MINW
+#define HJ_PLAN_MINW 6
+#endif
+
 
 
 namespace {
@@ -83,11 +97,11 @@ struct Plan {
 // modelled makespan  waves(T) * (T + overhead),  waves = ceil(tiles / slots),
 // over T in [4, 96] with at least `min_waves` waves when the batch allows it
 // (several waves even out the float64-fallback variance between tiles;
-// measured: 4:2:0 is best at 2, 4:4:4 / 4:2:2 at 4+).  A batch too small to
+// measured: 4:2:0 is best at 2, 4:4:4 / 4:2:2 at 6).  A batch too small to
 // fill one wave first gets narrower strips.
 int choose_rows_per_tile(const hj_image_t *images, int n, int sub, int direct, int S, int64_t slots) {
-    const double overhead = sub == HJ_SUB_420 ? 1.5 : 0.7;  // in steps
-    const int64_t min_waves = sub == HJ_SUB_420 ? 2 : 4;
+    const double overhead = sub == HJ_SUB_420 ? HJ_PLAN_OVH_420 : HJ_PLAN_OVH;  // in steps
+    const int64_t min_waves = sub == HJ_SUB_420 ? HJ_PLAN_MINW_420 : HJ_PLAN_MINW;
     int best_T = 8;
     double best = 1e300;
     for (int T = 4; T <= 96; ++T) {
