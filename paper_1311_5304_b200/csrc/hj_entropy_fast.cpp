@@ -26,7 +26,7 @@
 namespace {
 
 const int kZigzag[64] = HJ_ZIGZAG_INIT;
-constexpr int kLook = 9;
+constexpr int kLook = 11;
 
 // AC fast entry: bits 0-15 value (int16), 16-19 run, 20-24 consumed length,
 // 25-27 kind.
