@@ -180,10 +180,15 @@ __device__ __forceinline__ void ldg_rows2(const int4 *p, int4 &a, int4 &b) {
 #endif
 }
 
+#ifndef HJ_CVT_H1
+#define HJ_CVT_H1 0
+#endif
 // FP32 screen of one block: returns true (and the 64 samples, u8 row-major,
 // 4 per word) when every sample is proven equal to the reference's float64
-// result; false = recompute exactly.
-__device__ __forceinline__ bool screen_block(const int16_t *__restrict__ src, const float *qf,
+// result; false = recompute exactly.  Two f32x2 formulations of the same
+// operations: screen_rows (lanes = two columns in the column pass, 2x2
+// register transposes before the row pass) and screen_cols (aan_col below).
+__device__ __forceinline__ bool screen_rows(const int16_t *__restrict__ src, const float *qf,
                                              uint32_t (&out)[16]) {
     int4 raw[8];
     const int4 *s4 = reinterpret_cast<const int4 *>(src);
@@ -240,6 +245,125 @@ __device__ __forceinline__ bool screen_block(const int16_t *__restrict__ src, co
         out[r1 * 2 + 1] = pack4(n1[4], n1[5], n1[6], n1[7]);
     }
     return (acc >> 15) == 0;
+}
+
+// Column pass with the two f32x2 lanes inside ONE column transform (two rows
+// of the column per register), so that its outputs are already the row pairs
+// the row pass consumes: no 2x2 register transposes between the passes.
+// Every lane computes exactly the IEEE operation of aan_x2 on the same
+// operands (x*(+-1) + y inside an FMA is the rounded sum / difference), so
+// the screen's values - and its error bound - are unchanged.
+//   in:  A = (x0, x2)  B = (x4, x6)  C = (x5, x1)  D = (x3, x7)
+//   out: A = (y0, y3)  B = (y7, y4)  C = (y1, y2)  D = (y6, y5)
+__device__ __forceinline__ u64 bc(float x) { return pk(x, x); }
+// (1, -1), (-1, 1), (-ROT_M, -ROT_P) as constant-bank pairs: ptxas keeps them
+// in uniform registers and uses them as FFMA2 operands directly (built from
+// immediates they would be re-materialised into register pairs at each use)
+__constant__ __align__(8) float kColPairs[6] = {1.0f, -1.0f, -1.0f, 1.0f, -F_ROT_M, -F_ROT_P};
+__device__ __forceinline__ u64 col_pair(int i) { return reinterpret_cast<const u64 *>(kColPairs)[i]; }
+__device__ __forceinline__ void aan_col(u64 &A, u64 &B, u64 &C, u64 &D, u64 pm, u64 mp, u64 nrot) {
+    const u64 U = add2(A, B);   // (tmp10, tmp13)
+    const u64 V = sub2(A, B);   // (tmp11, d2 - d6)
+    const u64 Z1 = add2(C, D);  // (z13, z11)
+    const u64 Z2 = sub2(C, D);  // (z10, z12)
+    const float ntmp12 = fmaf(phi(V), -F_SQRT2, phi(U));
+    const u64 E03 = fma2(bc(phi(U)), pm, bc(plo(U)));   // (e0, e3) = tmp10 +- tmp13
+    const u64 E12 = fma2(bc(ntmp12), mp, bc(plo(V)));   // (e1, e2) = tmp11 -+ ntmp12
+    const u64 T7S = fma2(bc(plo(Z1)), pm, bc(phi(Z1))); // (t7, z11 - z13)
+    const float t11 = phi(T7S) * F_SQRT2;
+    const float z5 = (plo(Z2) + phi(Z2)) * F_ROT;
+    const u64 T12 = fma2(Z2, nrot, bc(z5));             // (t12, nt10)
+    const float t7 = plo(T7S);
+    const float t6 = plo(T12) - t7;
+    const float t5 = t11 - t6;
+    const float t4 = t5 - phi(T12);
+    const u64 T74 = pk(t7, t4), T65 = pk(t6, t5);
+    A = fma2(T74, pm, E03);  // (e0 + t7, e3 - t4)
+    B = fma2(T74, mp, E03);  // (e0 - t7, e3 + t4)
+    C = add2(E12, T65);      // (e1 + t6, e2 + t5)
+    D = sub2(E12, T65);      // (e1 - t6, e2 - t5)
+}
+
+// Shared-memory order of the binary32 dequantisation factors: row-major for
+// screen_rows; for screen_cols column c holds rows (0, 2, 4, 6, 5, 1, 3, 7)
+// at [8c, 8c + 8).
+__host__ __device__ constexpr int qf_slot(bool cols, int r, int c) {
+    return !cols ? 8 * r + c
+                 : 8 * c + (r == 0 ? 0 : r == 2 ? 1 : r == 4 ? 2 : r == 6 ? 3 : r == 5 ? 4 : r == 1 ? 5 : r == 3 ? 6 : 7);
+}
+
+__device__ __forceinline__ bool screen_cols(const int16_t *__restrict__ src, const float *qf,
+                                             uint32_t (&out)[16]) {
+    int4 raw[8];
+    const int4 *s4 = reinterpret_cast<const int4 *>(src);
+#pragma unroll
+    for (int r = 0; r < 8; r += 2) ldg_rows2(s4 + r, raw[r], raw[r + 1]);
+    const u64 pm = col_pair(0), mp = col_pair(1), nrot = col_pair(2);
+    u64 Y[8][4];  // Y[c][k]: column c, row pair k
+    float b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        float f[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int w = c < 2 ? raw[r].x : c < 4 ? raw[r].y : c < 6 ? raw[r].z : raw[r].w;
+#if HJ_CVT_H1
+            f[r] = (c & 1) ? (float)(short)((unsigned)w >> 16) : (float)(short)(w & 0xffff);
+#else
+            f[r] = (c & 1) ? (float)(w >> 16) : (float)(short)(w & 0xffff);
+#endif
+        }
+        const float4 qa = lds128f(qf + 8 * c), qb = lds128f(qf + 8 * c + 4);
+        u64 A = mul2(pk(f[0], f[2]), pk(qa.x, qa.y));
+        u64 B = mul2(pk(f[4], f[6]), pk(qa.z, qa.w));
+        u64 C = mul2(pk(f[5], f[1]), pk(qb.x, qb.y));
+        u64 D = mul2(pk(f[3], f[7]), pk(qb.z, qb.w));
+        b0 = fmaf(fabsf(plo(A)), kScreenK[0 * 8 + c], b0);
+        b1 = fmaf(fabsf(phi(A)), kScreenK[2 * 8 + c], b1);
+        b2 = fmaf(fabsf(plo(B)), kScreenK[4 * 8 + c], b2);
+        b3 = fmaf(fabsf(phi(B)), kScreenK[6 * 8 + c], b3);
+        b0 = fmaf(fabsf(plo(C)), kScreenK[5 * 8 + c], b0);
+        b1 = fmaf(fabsf(phi(C)), kScreenK[1 * 8 + c], b1);
+        b2 = fmaf(fabsf(plo(D)), kScreenK[3 * 8 + c], b2);
+        b3 = fmaf(fabsf(phi(D)), kScreenK[7 * 8 + c], b3);
+        aan_col(A, B, C, D, pm, mp, nrot);
+        Y[c][0] = A;
+        Y[c][1] = B;
+        Y[c][2] = C;
+        Y[c][3] = D;
+    }
+    const float eq = bracket((b0 + b1) + (b2 + b3));
+    const u64 cm = pk(384.5f - eq, 384.5f - eq), cpl = pk(384.5f + eq, 384.5f + eq);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        // row pairs (0,3) (7,4) (1,2) (6,5)
+        const int ra = k == 0 ? 0 : k == 1 ? 7 : k == 2 ? 1 : 6;
+        const int rb = k == 0 ? 3 : k == 1 ? 4 : k == 2 ? 2 : 5;
+        aan_x2(Y[0][k], Y[1][k], Y[2][k], Y[3][k], Y[4][k], Y[5][k], Y[6][k], Y[7][k]);
+        int n0[8], n1[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) round_pair(Y[c][k], cm, cpl, acc, n0[c], n1[c]);
+        out[ra * 2] = pack4(n0[0], n0[1], n0[2], n0[3]);
+        out[ra * 2 + 1] = pack4(n0[4], n0[5], n0[6], n0[7]);
+        out[rb * 2] = pack4(n1[0], n1[1], n1[2], n1[3]);
+        out[rb * 2 + 1] = pack4(n1[4], n1[5], n1[6], n1[7]);
+    }
+    return (acc >> 15) == 0;
+}
+
+// 4:4:4 / 4:2:2 take screen_cols (measured +4 % / +1 %); 4:2:0, whose kernel
+// sits at the 128-register cap with more live state, spills more with it
+// and keeps screen_rows (-8 % otherwise).
+#ifndef HJ_SCREEN_COLS_420
+#define HJ_SCREEN_COLS_420 0
+#endif
+template <int SUB>
+constexpr bool kScreenCols = SUB != HJ_SUB_420 || HJ_SCREEN_COLS_420;
+template <int SUB>
+__device__ __forceinline__ bool screen_block(const int16_t *__restrict__ src, const float *qf, uint32_t (&out)[16]) {
+    if constexpr (kScreenCols<SUB>) return screen_cols(src, qf, out);
+    else return screen_rows(src, qf, out);
 }
 
 // ------------------------------------------------------ exact fallback
@@ -307,6 +431,11 @@ struct Geo<HJ_SUB_420> {
     static constexpr int YSLOTS = 2;
     static constexpr int CROWS = 3 * 8 + 1;  // three MCU-row slots + the saved last row (index 24)
 };
+
+#ifndef HJ_CSTAGE
+#define HJ_CSTAGE 1
+#endif
+static_assert(sizeof(double) * 64 / 8 == 64, "exact staging holds 64 B per thread");
 
 template <int SUB>
 constexpr int kNT = threads_for(SUB);           // threads per CTA
@@ -565,7 +694,8 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
         const int q = im.q[i];
         sm.qi[i >> 6][i & 63] = q;
     }
-    for (int i = tid; i < 192; i += kThreads) sm.qf[i >> 6][i & 63] = (float)((double)im.q[i] * kPre64[i & 63]);
+    for (int i = tid; i < 192; i += kThreads)
+        sm.qf[i >> 6][qf_slot(kScreenCols<SUB>, (i & 63) >> 3, i & 7)] = (float)((double)im.q[i] * kPre64[i & 63]);
     if (tid == 0) sm.n_queue[0] = sm.n_queue[1] = sm.n_taken[0] = sm.n_taken[1] = 0;
 
     const int cm_lo = (SUB == HJ_SUB_444) ? t.m0 : t.m0 - 1;  // first chroma window MCU
@@ -678,7 +808,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     uint32_t w[16];
                     const int comp = is_y ? 0 : 1 + k;
                     bool ok = false;
-                    if (!direct) ok = screen_block(k ? srcB : srcA, sm.qf[comp], w);
+                    if (!direct) ok = screen_block<SUB>(k ? srcB : srcA, sm.qf[comp], w);
                     if (SUB == HJ_SUB_444 || is_y) {
                         // byte planes: Y (blocks side by side) or Cb / Cr
                         uint8_t *dst = is_y ? ydst + 8 * k : (k ? sm.crp[par] + 8 * lm : ydst);
@@ -688,10 +818,32 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                             push_exact(nq, queue, qdst, ((uint32_t)comp << 30) | (uint32_t)blk, k ? dB : dA);
                         }
                     } else if (k == 0) {
+#if HJ_CSTAGE
+                        // park block A's samples in this thread's 64 B of the
+                        // (phase-B-only) exact staging area: 16 registers
+                        // fewer live across the second screen
+                        if (!direct) {
+                            uint4 *st = reinterpret_cast<uint4 *>(&sm.g[0][0]) + 4 * tid;
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                sts128(st + i, make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]));
+                        }
+#else
 #pragma unroll
                         for (int i = 0; i < 16; ++i) keep[i] = w[i];
+#endif
                         okA = ok;
                     } else {
+#if HJ_CSTAGE
+                        if (!direct) {
+                            const uint4 *st = reinterpret_cast<const uint4 *>(&sm.g[0][0]) + 4 * tid;
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const uint4 v = lds128(st + i);
+                                keep[4 * i] = v.x, keep[4 * i + 1] = v.y, keep[4 * i + 2] = v.z, keep[4 * i + 3] = v.w;
+                            }
+                        }
+#endif
                         if (!direct) write_c16_rows(cdst, G::CW, keep, w);
                         const uint32_t blk = (uint32_t)((int64_t)crow * mpr + m);
                         if (!okA) push_exact(nq, queue, qdst, (1u << 30) | blk, dA);
