@@ -917,7 +917,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     uint32_t n3[10];
                     load_c10(pn, le, re, n3);
 #pragma unroll
-                    for (int k = 0; k < 10; ++k) n3[k] *= 3u << G::CSH;
+                    for (int k = 0; k < 10; ++k) n3[k] = n3[k] * (3u << G::CSH) + 0x00200020u;
                     const int rows = min(2, im.height - y0);
 #pragma unroll 1
                     for (int h = 0; h < rows; ++h) {
@@ -925,9 +925,11 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                         load_c10(h ? pd : pu, le, re, cs10);
 #pragma unroll
                         for (int k = 0; k < 10; ++k) cs10[k] = (cs10[k] << G::CSH) + n3[k];
-                        // even 16(3cs+prev+8), odd 16(3cs+next+7)
+                        // even 16(3cs+prev+8), odd 16(3cs+next+7): each colsum
+                        // carries +2 (x16) from n3, so 3cs+prev already holds
+                        // the +8 and odd subtracts 1 (lanes stay >= 0x80)
                         render16_swar(im.rgb + ((int64_t)(y0 + h) * im.width + x0) * 3,
-                                      lds128(yp + (2 * p + h) * G::YW + 16 * g), cs10, 0x00800080u, 0x00700070u,
+                                      lds128(yp + (2 * p + h) * G::YW + 16 * g), cs10, 0u, 0u - 0x00100010u,
                                       npx);
                     }
                 }
@@ -950,10 +952,11 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     uint32_t c10[10];
                     load_c10(crow0 + y * G::CW + 8 * (g + 1), left_edge && g == 0, right_edge && g == S - 1, c10);
 #pragma unroll
-                    for (int k = 0; k < 10; ++k) c10[k] <<= G::CSH;
-                    // h2v1 on 64x-scaled lanes: even 64(3c+prev+1), odd 64(3c+next+2)
+                    for (int k = 0; k < 10; ++k) c10[k] = (c10[k] << G::CSH) + 0x00100010u;
+                    // h2v1 on 64x-scaled lanes: even 64(3c+prev+1), odd 64(3c+next+2);
+                    // each sample carries +1/4 (x64), so 3c+prev already holds the +1
                     render16_swar(im.rgb + ((int64_t)yy * im.width + x0) * 3, lds128(yp + y * G::YW + 16 * g),
-                                  c10, 0x00400040u, 0x00800080u, npx);
+                                  c10, 0u, 0x00400040u, npx);
                 }
             } else {
                 // item = (MCU pair g, row y): 16 pixels
