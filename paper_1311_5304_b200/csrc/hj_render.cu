@@ -492,6 +492,13 @@ __device__ __forceinline__ void push_exact(int *n_queue, uint32_t *queue, uint32
     qdst[e] = dst;
 }
 
+// A block the screen could not prove is re-read by phase B's exact path; the
+// screen's own loads bypassed L1, so pull its line into L1 now.
+#ifndef HJ_PF_EXACT
+#define HJ_PF_EXACT 1
+#endif
+__device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 // Unaligned / cropped tail of a 16-pixel RGB row (rare: odd widths, right edge).
 __device__ __noinline__ void store_partial(uint8_t *__restrict__ dst, uint4 a, uint4 b, uint4 c, int nbytes) {
     const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
@@ -816,6 +823,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                         if (!ok) {
                             const int64_t blk = ((k ? srcB : srcA) - (is_y ? im.y : k ? im.cr : im.cb)) / 64;
                             push_exact(nq, queue, qdst, ((uint32_t)comp << 30) | (uint32_t)blk, k ? dB : dA);
+                            if (HJ_PF_EXACT) prefetch_l1(k ? srcB : srcA);
                         }
                     } else if (k == 0) {
 #if HJ_CSTAGE
@@ -846,8 +854,14 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
 #endif
                         if (!direct) write_c16_rows(cdst, G::CW, keep, w);
                         const uint32_t blk = (uint32_t)((int64_t)crow * mpr + m);
-                        if (!okA) push_exact(nq, queue, qdst, (1u << 30) | blk, dA);
-                        if (!ok) push_exact(nq, queue, qdst, (2u << 30) | blk, dB);
+                        if (!okA) {
+                            push_exact(nq, queue, qdst, (1u << 30) | blk, dA);
+                            if (HJ_PF_EXACT) prefetch_l1(srcA);
+                        }
+                        if (!ok) {
+                            push_exact(nq, queue, qdst, (2u << 30) | blk, dB);
+                            if (HJ_PF_EXACT) prefetch_l1(srcB);
+                        }
                     }
                 }
             }
