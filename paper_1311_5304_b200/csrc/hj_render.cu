@@ -183,6 +183,17 @@ __device__ __forceinline__ void ldg_rows2(const int4 *p, int4 &a, int4 &b) {
 #ifndef HJ_CVT_H1
 #define HJ_CVT_H1 0
 #endif
+// The 2x2 transposes between the passes as explicit PRMT copies: ptxas
+// otherwise emits IMAD.MOV, on the FMA pipe the screen already saturates.
+#ifndef HJ_PRMT_T
+#define HJ_PRMT_T 1
+#endif
+__device__ __forceinline__ float alu_mov(float x) {
+    uint32_t d;
+    asm volatile("prmt.b32 %0, %1, 0, 0x3210;" : "=r"(d) : "r"(__float_as_uint(x)));
+    return __uint_as_float(d);
+}
+
 // FP32 screen of one block: returns true (and the 64 samples, u8 row-major,
 // 4 per word) when every sample is proven equal to the reference's float64
 // result; false = recompute exactly.  Two f32x2 formulations of the same
@@ -233,7 +244,11 @@ __device__ __forceinline__ bool screen_rows(const int16_t *__restrict__ src, con
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             u64 a = X[j >> 1][r0], b = X[j >> 1][r1];
+#if HJ_PRMT_T
+            Q[j] = (j & 1) ? pk(alu_mov(phi(a)), alu_mov(phi(b))) : pk(alu_mov(plo(a)), alu_mov(plo(b)));
+#else
             Q[j] = (j & 1) ? pk(phi(a), phi(b)) : pk(plo(a), plo(b));
+#endif
         }
         aan_x2(Q[0], Q[1], Q[2], Q[3], Q[4], Q[5], Q[6], Q[7]);
         int n0[8], n1[8];
