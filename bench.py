@@ -259,8 +259,8 @@ def amdahl_run(images, wl, world, pg, n_images):
             "frac_of_bound": round(t_h / t_w, 4), "mpix_s": round(px / t_w / 1e6, 1),
             "huffman_mpix_s": round(px / t_h / 1e6, 1), "host_threads_per_rank": threads,
             "images_per_rank": n_images, "bit_exact_vs_oracle": exact,
-            "note": "T_huff = native host Huffman alone (same decoder/threads); T_wall = Huffman "
-                    "pipelined with H2D+render+D2H queued by each host worker on its own CUDA "
+            "note": "T_huff = native host Huffman alone (hj_pipeline_huffman, same decoder/threads); T_wall = Huffman "
+                    "pipelined with H2D+render+D2H queued by each native worker thread (hj_pipeline_run) on its own CUDA "
                     "stream; medians of 7 interleaved runs, max over ranks"}
 
 

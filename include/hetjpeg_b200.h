@@ -199,6 +199,33 @@ hj_status hj_decode_scan_fast(const void *fast, const uint8_t *data, int64_t n_b
                               int32_t mcus_per_row, int32_t mcu_rows, int32_t y_per_mcu,
                               int32_t restart_interval, int32_t n_threads);
 
+/* ---- native batch pipeline (pipeline.BatchDecoder; the paper's pipelined
+ * host-Huffman / accelerator scheme, §5.3, at batch granularity).
+ * One image: its scan (hj_huff_build tables + entropy-coded bytes), its
+ * page-locked host coefficient planes and RGB, its device planes / RGB and
+ * an hj_plan_create plan rendering it from those device planes. */
+typedef struct {
+    const void *huff;
+    const uint8_t *scan;
+    int64_t scan_bytes;
+    int16_t *y, *cb, *cr;                 /* host planes (page-locked) */
+    void *dev_y, *dev_cb, *dev_cr;        /* device planes */
+    int64_t n_y, n_c;                     /* blocks in the Y / each chroma plane */
+    int32_t mcus_per_row, mcu_rows, y_per_mcu, restart_interval;
+    void *plan;
+    const void *dev_rgb;
+    uint8_t *rgb;                         /* host RGB (page-locked) */
+    int64_t rgb_bytes;
+} hj_pipe_image_t;
+
+/* n_threads host threads each take the next image, entropy-decode it
+ * (hj_decode_scan_fast) and queue its H2D -> render -> D2H on streams[t];
+ * returns once every stream has drained (first error wins). */
+hj_status hj_pipeline_run(const hj_pipe_image_t *images, int32_t n_images, int32_t n_threads,
+                          void *const *streams);
+/* The same host stage alone (T_huff of the Amdahl bound, orchestrator.py:71-75). */
+hj_status hj_pipeline_huffman(const hj_pipe_image_t *images, int32_t n_images, int32_t n_threads);
+
 /* Index of the first non-restart marker after the scan data starting at
  * `start`, or -1 if the stream ends inside the entropy-coded data
  * (parser.py:277-293, _scan_entropy_end). */

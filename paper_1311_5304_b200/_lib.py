@@ -60,6 +60,18 @@ class hj_scan_tables_t(C.Structure):  # noqa: N801
     ]
 
 
+class hj_pipe_image_t(C.Structure):  # noqa: N801
+    _fields_ = [
+        ("huff", C.c_void_p), ("scan", C.c_void_p), ("scan_bytes", C.c_int64),
+        ("y", C.c_void_p), ("cb", C.c_void_p), ("cr", C.c_void_p),
+        ("dev_y", C.c_void_p), ("dev_cb", C.c_void_p), ("dev_cr", C.c_void_p),
+        ("n_y", C.c_int64), ("n_c", C.c_int64),
+        ("mcus_per_row", C.c_int32), ("mcu_rows", C.c_int32), ("y_per_mcu", C.c_int32),
+        ("restart_interval", C.c_int32),
+        ("plan", C.c_void_p), ("dev_rgb", C.c_void_p), ("rgb", C.c_void_p), ("rgb_bytes", C.c_int64),
+    ]
+
+
 if not os.path.exists(_LIB_PATH):
     raise ImportError(
         f"native library missing: {_LIB_PATH} (build it with "
@@ -111,6 +123,8 @@ _SIG = {
     "hj_huff_build": (C.c_int, [C.POINTER(hj_scan_tables_t), C.POINTER(_P)]),
     "hj_huff_free": (None, [_P]),
     "hj_decode_scan_fast": (C.c_int, [_P, _P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _I32]),
+    "hj_pipeline_run": (C.c_int, [C.POINTER(hj_pipe_image_t), _I32, _I32, C.POINTER(_P)]),
+    "hj_pipeline_huffman": (C.c_int, [C.POINTER(hj_pipe_image_t), _I32, _I32]),
 }
 for _name, (_res, _args) in _SIG.items():
     _fn = getattr(lib, _name)

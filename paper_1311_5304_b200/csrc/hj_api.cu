@@ -10,6 +10,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -421,6 +422,78 @@ hj_status hj_render_batch(const hj_image_t *images, int n_images, void *stream) 
 }
 
 uint64_t hj_launch_count(void) { return g_launches.load(); }
+
+// ---------------------------------------------------------------- pipeline
+
+// Native batch pipeline (pipeline.BatchDecoder): host threads pull images
+// from a shared counter, entropy-decode each into its page-locked planes and
+// queue that image's H2D -> render -> D2H on the thread's own stream, so the
+// GPU work of decoded images overlaps the Huffman decoding of the rest with
+// no Python (GIL) between the steps.
+static hj_status pipe_run(const hj_pipe_image_t *images, int32_t n_images, int32_t n_threads,
+                          void *const *streams, int gpu) {
+    if (n_images < 0 || (n_images > 0 && !images) || n_threads < 1 || (gpu && !streams)) return HJ_ERR_ARG;
+    if (n_images == 0) return HJ_OK;
+    int device = 0;
+    if (gpu && cudaGetDevice(&device) != cudaSuccess) return HJ_ERR_CUDA;
+    std::atomic<int> next{0};
+    std::atomic<int> first_err{HJ_OK};
+    auto worker = [&](int t) {
+        if (gpu) cudaSetDevice(device);
+        cudaStream_t st = gpu ? as_stream(streams[t]) : nullptr;
+        for (int i = next.fetch_add(1); i < n_images && first_err.load() == HJ_OK; i = next.fetch_add(1)) {
+            const hj_pipe_image_t &im = images[i];
+            hj_status s = hj_decode_scan_fast(im.huff, im.scan, im.scan_bytes, im.y, im.cb, im.cr, im.mcus_per_row,
+                                              im.mcu_rows, im.y_per_mcu, im.restart_interval, 1);
+            if (s == HJ_OK && gpu) {
+                cudaError_t e = cudaSuccess;
+                // [Y | Cb | Cr] contiguous on both sides (the CoefficientBuffer /
+                // DeviceBatch layouts): one copy, fewer driver calls per image
+                const bool packed = im.cb == im.y + im.n_y * 64 && im.cr == im.cb + im.n_c * 64 &&
+                                    static_cast<char *>(im.dev_cb) == static_cast<char *>(im.dev_y) + im.n_y * 128 &&
+                                    static_cast<char *>(im.dev_cr) == static_cast<char *>(im.dev_cb) + im.n_c * 128;
+                if (packed) {
+                    e = cudaMemcpyAsync(im.dev_y, im.y, (size_t)(im.n_y + 2 * im.n_c) * 128, cudaMemcpyHostToDevice, st);
+                } else {
+                    if (im.n_y) e = cudaMemcpyAsync(im.dev_y, im.y, (size_t)im.n_y * 128, cudaMemcpyHostToDevice, st);
+                    if (e == cudaSuccess && im.n_c)
+                        e = cudaMemcpyAsync(im.dev_cb, im.cb, (size_t)im.n_c * 128, cudaMemcpyHostToDevice, st);
+                    if (e == cudaSuccess && im.n_c)
+                        e = cudaMemcpyAsync(im.dev_cr, im.cr, (size_t)im.n_c * 128, cudaMemcpyHostToDevice, st);
+                }
+                s = e == cudaSuccess ? plan_launch(static_cast<Plan *>(im.plan), st) : cuda_fail(e, "pipeline h2d");
+                if (s == HJ_OK && im.rgb_bytes) {
+                    e = cudaMemcpyAsync(im.rgb, im.dev_rgb, (size_t)im.rgb_bytes, cudaMemcpyDeviceToHost, st);
+                    if (e != cudaSuccess) s = cuda_fail(e, "pipeline d2h");
+                }
+            }
+            if (s != HJ_OK) {
+                int expect = HJ_OK;
+                first_err.compare_exchange_strong(expect, (int)s);
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    pool.reserve((size_t)n_threads);
+    for (int t = 0; t < n_threads; ++t) pool.emplace_back(worker, t);
+    for (auto &th : pool) th.join();
+    if (gpu) {
+        for (int t = 0; t < n_threads; ++t) {
+            cudaError_t e = cudaStreamSynchronize(as_stream(streams[t]));
+            if (e != cudaSuccess && first_err.load() == HJ_OK) return cuda_fail(e, "pipeline sync");
+        }
+    }
+    return (hj_status)first_err.load();
+}
+
+hj_status hj_pipeline_run(const hj_pipe_image_t *images, int32_t n_images, int32_t n_threads,
+                          void *const *streams) {
+    return pipe_run(images, n_images, n_threads, streams, 1);
+}
+
+hj_status hj_pipeline_huffman(const hj_pipe_image_t *images, int32_t n_images, int32_t n_threads) {
+    return pipe_run(images, n_images, n_threads, nullptr, 0);
+}
 
 uint64_t hj_exact_block_count(void) { return hj::exact_block_count(); }
 

@@ -113,13 +113,63 @@ class BatchDecoder:
             self.batch.upload_qtables(i, self.q[i], self.streams[0])
             self.batch.render_items([(i, 0, self.geos[i].mcu_rows)], self.streams[0])  # cache the plans
         self.streams[0].synchronize()
+        self._native = self._pipe_descriptors()
+
+    def _pipe_descriptors(self):
+        """hj_pipe_image_t per image for the native pipeline (hj_pipeline_run)."""
+        import ctypes as C
+
+        import numpy as np
+        b = self.batch
+        arr = (_lib.hj_pipe_image_t * max(1, len(self.geos)))()
+        self._scan_views = []
+        for i, g in enumerate(self.geos):
+            sp = self.parsed[i].entropy_span
+            view = np.frombuffer(self.blobs[i], dtype=np.uint8)[sp.offset:sp.offset + sp.length]
+            self._scan_views.append(view)
+            c, slot = self.coeffs[i], b.slots[i]
+            d = arr[i]
+            d.huff = self.scans[i]._h
+            d.scan, d.scan_bytes = view.ctypes.data, len(view)
+            d.y, d.cb, d.cr = c.y_blocks.ctypes.data, c.cb_blocks.ctypes.data, c.cr_blocks.ctypes.data
+            d.dev_y, d.dev_cb, d.dev_cr = (b.coef.ptr + slot.y_off, b.coef.ptr + slot.cb_off,
+                                           b.coef.ptr + slot.cr_off)
+            d.n_y, d.n_c = len(c.y_blocks), len(c.cb_blocks)
+            d.mcus_per_row, d.mcu_rows, d.y_per_mcu = g.mcus_per_row, g.mcu_rows, g.y_blocks_per_mcu
+            d.restart_interval = self.parsed[i].restart_interval
+            d.plan = b._plans[((i, 0, g.mcu_rows),)]
+            d.dev_rgb = b.rgb.ptr + slot.rgb_off
+            d.rgb, d.rgb_bytes = self.pixels[i].data.ctypes.data, g.width * g.height * 3
+        handles = (C.c_void_p * len(self.streams))(*[s.handle for s in self.streams])
+        self._h2d = sum(2 * len(c.y_blocks) * 64 + 2 * 2 * len(c.cb_blocks) * 64 for c in self.coeffs)
+        self._d2h = sum(g.width * g.height * 3 for g in self.geos)
+        return arr, handles
 
     def _huff(self, i: int) -> int:
         self.scans[i].decode(self.blobs[i], out=self.coeffs[i], threads=1)
         return i
 
     def huffman_only(self) -> float:
-        """Wall seconds of the host entropy stage alone over the batch."""
+        """Wall seconds of the host entropy stage alone over the batch (native
+        threads, hj_pipeline_huffman: the same work as run() minus the GPU)."""
+        import time
+        arr, _ = self._native
+        t0 = time.perf_counter()
+        _lib.check(_lib.lib.hj_pipeline_huffman(arr, len(self.geos), self.threads), "pipeline huffman")
+        return time.perf_counter() - t0
+
+    def run(self) -> dict:
+        """Decode the whole batch into self.pixels (native pipeline,
+        hj_pipeline_run: no Python between an image's Huffman and its GPU work);
+        returns wall seconds and bytes moved."""
+        import time
+        arr, handles = self._native
+        t0 = time.perf_counter()
+        _lib.check(_lib.lib.hj_pipeline_run(arr, len(self.geos), self.threads, handles), "pipeline run")
+        return {"wall_s": time.perf_counter() - t0, "h2d_bytes": self._h2d, "d2h_bytes": self._d2h}
+
+    def huffman_only_threads(self) -> float:
+        """huffman_only() through a Python thread pool (comparison)."""
         import time
         from concurrent.futures import ThreadPoolExecutor
         t0 = time.perf_counter()
@@ -127,8 +177,9 @@ class BatchDecoder:
             list(ex.map(self._huff, range(len(self.blobs))))
         return time.perf_counter() - t0
 
-    def run(self) -> dict:
-        """Decode the whole batch into self.pixels; returns wall seconds and bytes moved."""
+    def run_threads(self) -> dict:
+        """run() through a Python thread pool, one ctypes call per step
+        (comparison: the GIL between the calls costs small images)."""
         import threading
         import time
         from concurrent.futures import ThreadPoolExecutor

@@ -78,5 +78,16 @@ def test_batch_decoder_pipelined_matches_reference():
             assert np.array_equal(px.data, c.rgb), c.name
         assert t_h > 0 and io["wall_s"] > 0
         assert io["d2h_bytes"] == sum(c.width * c.height * 3 for c in cases)
+        # the Python-thread form of the same pipeline agrees (and repeated
+        # native runs over the same buffers stay exact)
+        for px in dec.pixels:
+            px.data[...] = 0
+        dec.run_threads()
+        assert all(np.array_equal(px.data, c.rgb) for c, px in zip(cases, dec.pixels))
+        for px in dec.pixels:
+            px.data[...] = 0
+        dec.run()
+        assert all(np.array_equal(px.data, c.rgb) for c, px in zip(cases, dec.pixels))
+        assert dec.huffman_only_threads() > 0
     finally:
         dec.close()
