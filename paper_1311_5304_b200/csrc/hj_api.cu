@@ -100,6 +100,16 @@ struct Plan {
 // (several waves even out the float64-fallback variance between tiles;
 // measured: 4:2:0 is best at 2, 4:4:4 / 4:2:2 at 6).  A batch too small to
 // fill one wave first gets narrower strips.
+// Strips per image row for strip width S (MCUs).  4:4:4 pixel items cover
+// MCU pairs, so its strips are cut on pair boundaries (at most S/2 pairs).
+static int64_t strips_of(int mpr, int S, int sub) {
+    if (sub == HJ_SUB_444) {
+        const int64_t per = std::max(1, S / 2), nu = (mpr + 1) / 2;
+        return (nu + per - 1) / per;
+    }
+    return (mpr + S - 1) / S;
+}
+
 int choose_rows_per_tile(const hj_image_t *images, int n, int sub, int direct, int S, int64_t slots) {
     const double overhead = sub == HJ_SUB_420 ? HJ_PLAN_OVH_420 : HJ_PLAN_OVH;  // in steps
     const int64_t min_waves = sub == HJ_SUB_420 ? HJ_PLAN_MINW_420 : HJ_PLAN_MINW;
@@ -110,7 +120,7 @@ int choose_rows_per_tile(const hj_image_t *images, int n, int sub, int direct, i
         for (int i = 0; i < n; ++i) {
             const hj_image_t &im = images[i];
             if (im.subsampling != sub || ((im.flags & HJ_FLAG_DIRECT_IDCT) != 0) != (direct != 0)) continue;
-            tiles += (int64_t)((im.mcus_per_row + S - 1) / S) * ((im.n_rows + T - 1) / T);
+            tiles += strips_of(im.mcus_per_row, S, sub) * ((im.n_rows + T - 1) / T);
         }
         if (tiles == 0) return best_T;
         const int64_t waves = (tiles + slots - 1) / slots;
@@ -139,7 +149,7 @@ void build_tiles(const hj_image_t *images, int n, std::vector<hj::Tile> &tiles,
                 for (int i = 0; i < n; ++i) {
                     const hj_image_t &im = images[i];
                     if (im.subsampling != sub || ((im.flags & HJ_FLAG_DIRECT_IDCT) != 0) != (direct != 0)) continue;
-                    const int64_t ns = (im.mcus_per_row + S - 1) / S;
+                    const int64_t ns = strips_of(im.mcus_per_row, S, sub);
                     strips += ns;
                     strip_rows += ns * im.n_rows;
                 }
@@ -153,14 +163,20 @@ void build_tiles(const hj_image_t *images, int n, std::vector<hj::Tile> &tiles,
             for (int i = 0; i < n; ++i) {
                 const hj_image_t &im = images[i];
                 if (im.subsampling != sub || ((im.flags & HJ_FLAG_DIRECT_IDCT) != 0) != (direct != 0)) continue;
-                const int ns = (im.mcus_per_row + S - 1) / S;
+                const int ns = (int)strips_of(im.mcus_per_row, S, sub);
                 for (int r = im.row0; r < im.row0 + im.n_rows; r += T) {
                     int r1 = std::min(im.row0 + im.n_rows, r + T);
+                    // 4:4:4 pixel items cover MCU pairs: split on pair
+                    // boundaries so only the image's own right edge can end
+                    // in a half item (a half item sends its whole warp
+                    // through the partial-store path)
+                    const int unit = sub == HJ_SUB_444 ? 2 : 1;
+                    const int64_t nu = (im.mcus_per_row + unit - 1) / unit;
                     for (int s = 0; s < ns; ++s) {
                         hj::Tile t{};
                         t.image = i;
-                        t.m0 = (int)((int64_t)s * im.mcus_per_row / ns);
-                        t.m1 = (int)((int64_t)(s + 1) * im.mcus_per_row / ns);
+                        t.m0 = (int)std::min<int64_t>(im.mcus_per_row, unit * ((int64_t)s * nu / ns));
+                        t.m1 = (int)std::min<int64_t>(im.mcus_per_row, unit * ((int64_t)(s + 1) * nu / ns));
                         t.r0 = r;
                         t.r1 = r1;
                         tiles.push_back(t);

@@ -585,6 +585,12 @@ __device__ __forceinline__ void store48(uint8_t *__restrict__ dst, const uint32_
             *reinterpret_cast<uint16_t *>(dst + 45) = (uint16_t)(w[11] >> 8);
             dst[47] = (uint8_t)(w[11] >> 24);
         }
+    } else if (npx == 8 && (a & 7) == 0) {
+        // half item (4:4:4 image whose width is 8 mod 16): 24 bytes, 8-aligned
+        uint2 *d = reinterpret_cast<uint2 *>(dst);
+        d[0] = make_uint2(w[0], w[1]);
+        d[1] = make_uint2(w[2], w[3]);
+        d[2] = make_uint2(w[4], w[5]);
     } else {
         store_partial(dst, make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]),
                       make_uint4(w[8], w[9], w[10], w[11]), npx * 3);
