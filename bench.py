@@ -228,14 +228,14 @@ def cpu_baseline(images, wl, budget_s=3.0):
                       "(oracle/render_oracle.c, float64 AAN as the reference)"}
 
 
-def amdahl_run(images, wl, world, pg, n_images):
+def amdahl_run(images, wl, world, pg, n_images, reserve=0):
     """Full decode of a batch (host Huffman on this rank's share of the host
     cores, pipelined with H2D -> kernel -> D2H on the B200) against the
     Huffman stage alone with the same decoder and threads:
     frac = T_huff / T_wall = achieved fraction of the Amdahl-bound speedup
     (orchestrator.py:71-75, §6.4)."""
     from paper_1311_5304_b200.pipeline import BatchDecoder
-    threads = max(1, len(os.sched_getaffinity(0)) // world)
+    threads = max(1, len(os.sched_getaffinity(0)) // world - reserve)
     blobs = [images[i % len(images)][0] for i in range(n_images)]
     dec = BatchDecoder(blobs, threads=threads, n_streams=4)
     try:
@@ -588,6 +588,14 @@ def main():
     amdahl = None
     if not args.no_amdahl:
         amdahl = amdahl_run(images, wl, world, pg, args.amdahl_images)
+        # the same with one host core left to the GPU submission thread and
+        # the driver (both legs on the remaining cores): all-cores Huffman
+        # is fastest, but its workers then get preempted by the pipeline
+        cores = len(os.sched_getaffinity(0)) // world
+        if cores > 2:
+            r = amdahl_run(images, wl, world, pg, args.amdahl_images, reserve=1)
+            amdahl["one_core_reserved"] = {k: r[k] for k in ("t_huff_ms", "t_wall_ms", "frac_of_bound",
+                                                             "mpix_s", "host_threads_per_rank")}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:

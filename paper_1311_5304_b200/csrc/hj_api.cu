@@ -6,6 +6,8 @@
 // nothing but this library (ctypes, cgo, JNI ...).
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -446,52 +448,102 @@ uint64_t hj_launch_count(void) { return g_launches.load(); }
 // queue that image's H2D -> render -> D2H on the thread's own stream, so the
 // GPU work of decoded images overlaps the Huffman decoding of the rest with
 // no Python (GIL) between the steps.
+// Queue one decoded image's H2D -> render -> D2H on stream st.
+static hj_status pipe_submit(const hj_pipe_image_t &im, cudaStream_t st) {
+    cudaError_t e = cudaSuccess;
+    // [Y | Cb | Cr] contiguous on both sides (the CoefficientBuffer /
+    // DeviceBatch layouts): one copy, fewer driver calls per image
+    const bool packed = im.cb == im.y + im.n_y * 64 && im.cr == im.cb + im.n_c * 64 &&
+                        static_cast<char *>(im.dev_cb) == static_cast<char *>(im.dev_y) + im.n_y * 128 &&
+                        static_cast<char *>(im.dev_cr) == static_cast<char *>(im.dev_cb) + im.n_c * 128;
+    if (packed) {
+        e = cudaMemcpyAsync(im.dev_y, im.y, (size_t)(im.n_y + 2 * im.n_c) * 128, cudaMemcpyHostToDevice, st);
+    } else {
+        if (im.n_y) e = cudaMemcpyAsync(im.dev_y, im.y, (size_t)im.n_y * 128, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess && im.n_c)
+            e = cudaMemcpyAsync(im.dev_cb, im.cb, (size_t)im.n_c * 128, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess && im.n_c)
+            e = cudaMemcpyAsync(im.dev_cr, im.cr, (size_t)im.n_c * 128, cudaMemcpyHostToDevice, st);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "pipeline h2d");
+    hj_status s = plan_launch(static_cast<Plan *>(im.plan), st);
+    if (s == HJ_OK && im.rgb_bytes) {
+        e = cudaMemcpyAsync(im.rgb, im.dev_rgb, (size_t)im.rgb_bytes, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) s = cuda_fail(e, "pipeline d2h");
+    }
+    return s;
+}
+
+// The Huffman workers never enter the CUDA driver: each decoded image is
+// handed to the calling thread, which queues its GPU work round-robin over
+// the streams (HJ_PIPELINE_SUBMITTER=0: every worker queues its own images
+// on its own stream instead).
+static bool pipe_use_submitter() {
+    static const bool v = [] {
+        const char *e = std::getenv("HJ_PIPELINE_SUBMITTER");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 static hj_status pipe_run(const hj_pipe_image_t *images, int32_t n_images, int32_t n_threads,
                           void *const *streams, int gpu) {
     if (n_images < 0 || (n_images > 0 && !images) || n_threads < 1 || (gpu && !streams)) return HJ_ERR_ARG;
     if (n_images == 0) return HJ_OK;
     int device = 0;
     if (gpu && cudaGetDevice(&device) != cudaSuccess) return HJ_ERR_CUDA;
+    const bool submitter = gpu && pipe_use_submitter();
     std::atomic<int> next{0};
     std::atomic<int> first_err{HJ_OK};
+    auto record = [&](hj_status s) {
+        if (s != HJ_OK) {
+            int expect = HJ_OK;
+            first_err.compare_exchange_strong(expect, (int)s);
+        }
+    };
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<int> ready;
+    int finished = 0;  // images whose Huffman stage ended (ok or not)
     auto worker = [&](int t) {
-        if (gpu) cudaSetDevice(device);
-        cudaStream_t st = gpu ? as_stream(streams[t]) : nullptr;
-        for (int i = next.fetch_add(1); i < n_images && first_err.load() == HJ_OK; i = next.fetch_add(1)) {
+        if (gpu && !submitter) cudaSetDevice(device);
+        for (int i = next.fetch_add(1); i < n_images; i = next.fetch_add(1)) {
             const hj_pipe_image_t &im = images[i];
-            hj_status s = hj_decode_scan_fast(im.huff, im.scan, im.scan_bytes, im.y, im.cb, im.cr, im.mcus_per_row,
-                                              im.mcu_rows, im.y_per_mcu, im.restart_interval, 1);
-            if (s == HJ_OK && gpu) {
-                cudaError_t e = cudaSuccess;
-                // [Y | Cb | Cr] contiguous on both sides (the CoefficientBuffer /
-                // DeviceBatch layouts): one copy, fewer driver calls per image
-                const bool packed = im.cb == im.y + im.n_y * 64 && im.cr == im.cb + im.n_c * 64 &&
-                                    static_cast<char *>(im.dev_cb) == static_cast<char *>(im.dev_y) + im.n_y * 128 &&
-                                    static_cast<char *>(im.dev_cr) == static_cast<char *>(im.dev_cb) + im.n_c * 128;
-                if (packed) {
-                    e = cudaMemcpyAsync(im.dev_y, im.y, (size_t)(im.n_y + 2 * im.n_c) * 128, cudaMemcpyHostToDevice, st);
-                } else {
-                    if (im.n_y) e = cudaMemcpyAsync(im.dev_y, im.y, (size_t)im.n_y * 128, cudaMemcpyHostToDevice, st);
-                    if (e == cudaSuccess && im.n_c)
-                        e = cudaMemcpyAsync(im.dev_cb, im.cb, (size_t)im.n_c * 128, cudaMemcpyHostToDevice, st);
-                    if (e == cudaSuccess && im.n_c)
-                        e = cudaMemcpyAsync(im.dev_cr, im.cr, (size_t)im.n_c * 128, cudaMemcpyHostToDevice, st);
+            hj_status s = first_err.load() == HJ_OK
+                              ? hj_decode_scan_fast(im.huff, im.scan, im.scan_bytes, im.y, im.cb, im.cr,
+                                                    im.mcus_per_row, im.mcu_rows, im.y_per_mcu, im.restart_interval, 1)
+                              : HJ_OK;
+            record(s);
+            if (submitter) {
+                {
+                    std::lock_guard<std::mutex> g(mu);
+                    if (s == HJ_OK) ready.push_back(i);
+                    ++finished;
                 }
-                s = e == cudaSuccess ? plan_launch(static_cast<Plan *>(im.plan), st) : cuda_fail(e, "pipeline h2d");
-                if (s == HJ_OK && im.rgb_bytes) {
-                    e = cudaMemcpyAsync(im.rgb, im.dev_rgb, (size_t)im.rgb_bytes, cudaMemcpyDeviceToHost, st);
-                    if (e != cudaSuccess) s = cuda_fail(e, "pipeline d2h");
-                }
-            }
-            if (s != HJ_OK) {
-                int expect = HJ_OK;
-                first_err.compare_exchange_strong(expect, (int)s);
+                cv.notify_one();
+            } else if (s == HJ_OK && gpu && first_err.load() == HJ_OK) {
+                record(pipe_submit(im, as_stream(streams[t])));
             }
         }
     };
     std::vector<std::thread> pool;
     pool.reserve((size_t)n_threads);
     for (int t = 0; t < n_threads; ++t) pool.emplace_back(worker, t);
+    if (submitter) {
+        int done = 0, k = 0;
+        std::vector<int> batch;
+        while (done < n_images) {
+            {
+                std::unique_lock<std::mutex> g(mu);
+                cv.wait(g, [&] { return !ready.empty() || finished == n_images; });
+                batch.swap(ready);
+                done = finished;
+            }
+            for (int i : batch)
+                if (first_err.load() == HJ_OK) record(pipe_submit(images[i], as_stream(streams[k++ % n_threads])));
+            batch.clear();
+        }
+    }
     for (auto &th : pool) th.join();
     if (gpu) {
         for (int t = 0; t < n_threads; ++t) {
