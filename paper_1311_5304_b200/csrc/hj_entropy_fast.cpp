@@ -5,10 +5,12 @@
 // predictor wrap to int16, restart handling and error conditions), but
 //   * keeps a left-aligned 64-bit bit buffer refilled up to 56 bits at a time
 //     (stops at any marker, like _refill, _native.pyx:74-88);
-//   * decodes with 10-bit lookahead tables; for AC, one lookup yields code
-//     length + run + the EXTENDed value whenever code + magnitude bits fit in
-//     10 bits (most coefficients), else falls back to the canonical
-//     maxcode walk (_native.pyx:124-132);
+//   * decodes with 11-bit lookahead tables; for DC and AC, one lookup yields
+//     code length (+ run) + the EXTENDed value whenever code + magnitude bits
+//     fit in 11 bits (most coefficients), else the code alone with the
+//     magnitude bits read straight from the buffer; codes longer than 11 bits
+//     continue the canonical maxcode walk (_native.pyx:124-132) on the
+//     buffered bits;
 //   * splits a scan at its restart markers and decodes the intervals on
 //     several host threads - exact, because every RSTn resets the DC
 //     predictors (_native.pyx:238-257).
@@ -62,7 +64,18 @@ void build_table(const hj_scan_tables_t *s, int slot, Table &t, bool ac) {
             int lo = code << (kLook - len), n = 1 << (kLook - len);
             for (int v = lo; v < lo + n; ++v) {
                 t.look[v] = (uint16_t)((len << 8) | sym);
-                if (!ac) continue;
+                if (!ac) {
+                    // DC: the symbol is the magnitude category; > 15 is a bad
+                    // code (left to the generic path)
+                    int32_t e = kSlow << 25;
+                    if (sym == 0) e = kCoef << 25 | len << 20;
+                    else if (sym <= 15 && len + sym <= kLook)
+                        e = kCoef << 25 | (len + sym) << 20 |
+                            (extend((v >> (kLook - len - sym)) & ((1 << sym) - 1), sym) & 0xffff);
+                    else if (sym <= 15) e = kCodeOnly << 25 | len << 20 | sym;
+                    t.ac[v] = e;
+                    continue;
+                }
                 int r = sym >> 4, sz = sym & 15;
                 int32_t e;
                 if (sz == 0) {
@@ -149,6 +162,19 @@ inline int decode_sym(Reader &br, const Table &t, int &err) {
             return e & 0xff;
         }
     }
+    if (br.nbits >= 16) {
+        // no code of <= kLook bits prefixes the stream (the table): walk the
+        // longer lengths on the buffered bits (_native.pyx:124-132 order)
+        for (int l = kLook + 1; l < 17; ++l) {
+            const int code = (int)br.peek(l);
+            if (t.maxcode[l] >= 0 && code <= t.maxcode[l]) {
+                br.skip(l);
+                return t.symbols[t.valptr[l] + code - t.mincode[l]];
+            }
+        }
+        err = HJ_ERR_BADCODE;
+        return 0;
+    }
     int code = 0;
     for (int l = 1; l < 17; ++l) {
         int bit;
@@ -166,14 +192,26 @@ inline int decode_sym(Reader &br, const Table &t, int &err) {
 inline int decode_block(Reader &br, const Table &dc, const Table &ac, int16_t *out, int64_t &pred) {
     std::memset(out, 0, 64 * sizeof(int16_t));  // the block is about to be hot anyway
     int err = HJ_OK;
-    int t = decode_sym(br, dc, err);
-    if (err) return err;
-    if (t > 15) return HJ_ERR_BADCODE;
     int diff = 0;
-    if (t) {
-        int v;
-        if (!br.take(t, v)) return HJ_ERR_EXHAUSTED;
-        diff = extend(v, t);
+    if (br.nbits < 32) br.refill();
+    const int32_t de = br.nbits >= 32 ? dc.ac[br.peek(kLook)] : 0;
+    if ((de >> 25) == kCoef) {
+        br.skip((de >> 20) & 31);
+        diff = (int16_t)(de & 0xffff);
+    } else if ((de >> 25) == kCodeOnly) {
+        const int t = de & 0xff;  // 1..15; >= 16 buffered bits remain
+        br.skip((de >> 20) & 31);
+        diff = extend((int)br.peek(t), t);
+        br.skip(t);
+    } else {
+        int t = decode_sym(br, dc, err);
+        if (err) return err;
+        if (t > 15) return HJ_ERR_BADCODE;
+        if (t) {
+            int v;
+            if (!br.take(t, v)) return HJ_ERR_EXHAUSTED;
+            diff = extend(v, t);
+        }
     }
     pred += diff;
     out[0] = (int16_t)pred;
@@ -198,6 +236,17 @@ inline int decode_block(Reader &br, const Table &dc, const Table &ac, int16_t *o
             if (kind == kZrl) {
                 br.skip(len);
                 k += 16;
+                continue;
+            }
+            if (kind == kCodeOnly && br.nbits >= 32) {
+                // code in the table, magnitude bits past it: still buffered
+                const int r = (e >> 4) & 15, sz = e & 15;
+                br.skip(len);
+                k += r;
+                if (k > 63) return HJ_ERR_BADCODE;
+                out[kZigzag[k]] = (int16_t)extend((int)br.peek(sz), sz);
+                br.skip(sz);
+                ++k;
                 continue;
             }
         }
