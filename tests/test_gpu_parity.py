@@ -148,9 +148,10 @@ def _synthetic(width, height, quality, sub, **kw):
     (1023, 769, 85, "422", {"restart_blocks": 5}),
     (1001, 999, 80, "420", {}),
     (1922, 700, 70, "444", {}),   # rows start 2 bytes off a word: funnel-shifted stores
+    (1928, 300, 80, "444", {}),   # width 8 mod 16: every row ends in a 24-byte half item
     (1925, 300, 60, "422", {}),   # rows at every byte offset
 ], ids=["512_420", "1080p_420", "4096_444", "4096_422", "24MP_420_rst", "odd_422", "odd_420", "w2mod4_444",
-        "w1mod4_422"])
+        "w8mod16_444", "w1mod4_422"])
 def test_full_size_against_oracle(w, h, q, sub, kw):
     from paper_1311_5304_b200.block_transforms import alloc_pixels, render_rows
     p, coeffs, qt = _synthetic(w, h, q, sub, **kw)
