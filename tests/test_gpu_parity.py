@@ -248,3 +248,37 @@ def _lib_memset_poison(db):
     from paper_1311_5304_b200 import _lib
     _lib.check(_lib.lib.hj_memset_device(db.coef.ptr, 0x5A, db.coef.nbytes, None), "poison")
     _lib.check(_lib.lib.hj_device_synchronize(), "sync")
+
+
+@pytest.mark.parametrize("sub", ["444", "422", "420"])
+def test_strip_widths_sweep(cuda, sub):
+    """Widths around every strip / MCU-pair boundary, rendered as one small
+    batch (narrowed strips) and one image at a time, against the oracle:
+    the tile planner must cover every MCU column exactly once."""
+    from paper_1311_5304_b200 import device, entropy, parser
+    from paper_1311_5304_b200.perf_model import qtable_stack
+    from paper_1311_5304_b200.synth import synth_jpeg
+    widths = [8, 16, 24, 40, 72, 88, 168, 328, 336, 344, 352, 680, 696, 1000]
+    imgs = []
+    for k, w in enumerate(widths):
+        blob = synth_jpeg(w, 40, 70 + k, sub, seed=k)
+        p = parser.parse_stream(blob)
+        c, _ = entropy.decode_all(p, blob)
+        imgs.append((c, qtable_stack(p)))
+    code = {"444": 0, "422": 1, "420": 2}[sub]
+    for group in (list(range(len(imgs))), [len(imgs) - 1], [0]):
+        batch = device.DeviceBatch([imgs[i][0].geometry for i in group])
+        s = device.Stream()
+        for j, i in enumerate(group):
+            batch.upload_coefficients(j, imgs[i][0], s)
+            batch.upload_qtables(j, imgs[i][1], s)
+        batch.render(stream=s)
+        for j, i in enumerate(group):
+            c, q = imgs[i]
+            g = c.geometry
+            out = np.zeros((g.height, g.width, 3), np.uint8)
+            batch.download_rgb(j, out, s)
+            s.synchronize()
+            want = oracle.render(c.y_blocks, c.cb_blocks, c.cr_blocks, q, g.width, g.height, code, True)
+            assert np.array_equal(out, want), (sub, g.width)
+        batch.close()
