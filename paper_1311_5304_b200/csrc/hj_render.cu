@@ -373,8 +373,11 @@ __device__ __forceinline__ bool screen_cols(const int16_t *__restrict__ src, con
 #ifndef HJ_SCREEN_COLS_420
 #define HJ_SCREEN_COLS_420 0
 #endif
+#ifndef HJ_SCREEN_COLS
+#define HJ_SCREEN_COLS 1
+#endif
 template <int SUB>
-constexpr bool kScreenCols = SUB != HJ_SUB_420 || HJ_SCREEN_COLS_420;
+constexpr bool kScreenCols = (SUB != HJ_SUB_420 && HJ_SCREEN_COLS) || HJ_SCREEN_COLS_420;
 template <int SUB>
 __device__ __forceinline__ bool screen_block(const int16_t *__restrict__ src, const float *qf, uint32_t (&out)[16]) {
     if constexpr (kScreenCols<SUB>) return screen_cols(src, qf, out);
