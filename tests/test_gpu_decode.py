@@ -91,3 +91,29 @@ def test_batch_decoder_pipelined_matches_reference():
         assert dec.huffman_only_threads() > 0
     finally:
         dec.close()
+
+
+def test_batch_decoder_reports_a_truncated_scan():
+    """A scan cut short by an EOI in the middle of the entropy data: the
+    native pipeline's Huffman workers stop and the error surfaces as one of
+    the reference's exceptions (BitstreamExhausted / BadCode); a batch of
+    intact images afterwards decodes exactly."""
+    from paper_1311_5304_b200.errors import HetJpegError
+    good = max(GOLDEN_CASES, key=lambda c: c.width * c.height)
+    p = parser.parse_stream(good.jpeg)
+    sp = p.entropy_span
+    cut = good.jpeg[:sp.offset + sp.length // 2] + b"\xff\xd9"
+    dec = BatchDecoder([good.jpeg, cut], threads=2, n_streams=2)
+    try:
+        with pytest.raises(HetJpegError):
+            dec.run()
+        with pytest.raises(HetJpegError):
+            dec.huffman_only()
+    finally:
+        dec.close()
+    dec = BatchDecoder([good.jpeg], threads=1)
+    try:
+        dec.run()
+        assert np.array_equal(dec.pixels[0].data, good.rgb)
+    finally:
+        dec.close()
