@@ -832,7 +832,6 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                 // A's samples stay in `keep` until B is done
                 uint32_t keep[16];
                 bool okA = false;
-                if (has_b && !direct) asm volatile("prefetch.global.L1 [%0];" ::"l"(srcB));
 #pragma unroll 1
                 for (int k = 0; k < 2; ++k) {
                     if (k == 1 && !has_b) break;
