@@ -453,6 +453,9 @@ struct Geo<HJ_SUB_420> {
 #ifndef HJ_CSTAGE
 #define HJ_CSTAGE 1
 #endif
+#ifndef HJ_PF_L2
+#define HJ_PF_L2 1
+#endif
 static_assert(sizeof(double) * 64 / 8 == 64, "exact staging holds 64 B per thread");
 
 template <int SUB>
@@ -755,14 +758,14 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
             sm.n_queue[par ^ 1] = 0;  // last used in step s-1, next in s+1
             sm.n_taken[par ^ 1] = 0;
             // bulk L2 prefetch of the next step's coefficient ranges
-            const int ny = s + 1;
+            const int ny = HJ_PF_L2 ? s + 1 : -1;
             if (ny >= t.r0 && ny < t.r1) {
                 const int64_t b0 = ((int64_t)ny * mpr + t.m0) * YB;
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(im.y + b0 * 64),
                              "r"((unsigned)(S * YB * 128)));
             }
             const int nc = crow + 1;
-            if (nc < mcu_rows && nc <= t.r1) {
+            if (HJ_PF_L2 && nc < mcu_rows && nc <= t.r1) {
                 const int c0 = max(cm_lo, 0), c1 = min(cm_lo + n_cm, mpr);
                 const int64_t b0 = (int64_t)nc * mpr + c0;
                 const unsigned bytes = (unsigned)((c1 - c0) * 128);
