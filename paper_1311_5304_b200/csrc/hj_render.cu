@@ -576,8 +576,20 @@ __device__ __forceinline__ void store48(uint8_t *__restrict__ dst, const uint32_
         uint32_t *d = reinterpret_cast<uint32_t *>(dst - m);
         const unsigned sh = 8u * (unsigned)m;
         // word k of the aligned span = bytes of w[k-1] (high part) | w[k] (low part)
+        uint32_t f[12];
 #pragma unroll
-        for (int k = 1; k < 12; ++k) d[k] = __funnelshift_l(w[k - 1], w[k], sh);
+        for (int k = 1; k < 12; ++k) f[k] = __funnelshift_l(w[k - 1], w[k], sh);
+        // the 11 interior words as 8-byte stores where the span allows (a
+        // row's items share one alignment: 48-byte steps)
+        if ((reinterpret_cast<uintptr_t>(d + 1) & 7) == 0) {
+#pragma unroll
+            for (int k = 1; k < 11; k += 2) *reinterpret_cast<uint2 *>(d + k) = make_uint2(f[k], f[k + 1]);
+            d[11] = f[11];
+        } else {
+            d[1] = f[1];
+#pragma unroll
+            for (int k = 2; k < 12; k += 2) *reinterpret_cast<uint2 *>(d + k) = make_uint2(f[k], f[k + 1]);
+        }
         // head: the first 4-m bytes of w[0]; tail: the last m bytes of w[11]
         if (m == 2) {
             *reinterpret_cast<uint16_t *>(dst) = (uint16_t)w[0];
