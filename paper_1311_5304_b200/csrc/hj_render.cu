@@ -568,9 +568,12 @@ __device__ __forceinline__ void store48(uint8_t *__restrict__ dst, const uint32_
 #pragma unroll
         for (int i = 0; i < 6; ++i) d[i] = make_uint2(w[2 * i], w[2 * i + 1]);
     } else if (npx == 16 && (a & 3) == 0) {
+        // a = 4 mod 8: one word, five 8-byte pairs, one word
         uint32_t *d = reinterpret_cast<uint32_t *>(dst);
+        d[0] = w[0];
 #pragma unroll
-        for (int i = 0; i < 12; ++i) d[i] = w[i];
+        for (int i = 1; i < 11; i += 2) *reinterpret_cast<uint2 *>(d + i) = make_uint2(w[i], w[i + 1]);
+        d[11] = w[11];
     } else if (npx == 16) {
         const int m = (int)(a & 3);  // 1..3
         uint32_t *d = reinterpret_cast<uint32_t *>(dst - m);
