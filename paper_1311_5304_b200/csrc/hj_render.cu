@@ -3,24 +3,28 @@
 // (kernels/_native.pyx:312-549, kernels/fallback.py:37-260).
 //
 // IDCT numerics: every block is first transformed
-// in binary32 with the reference's AAN operation order.  A thread screens
-// TWO blocks at once, block A in the low and block B in the high lane of
-// every f32x2 register, so both 1-D passes run as FADD2/FFMA2 with no
-// register transposes.  A rigorous first-order error bound
-// E = u * sum_i K_i |x_i| (K from tools/analysis/screen_constants.py)
-// brackets each sample; if no rounding boundary of floor(s + 128.5) lies
-// inside [s - E, s + E] for all 64 samples, the binary32 result provably
-// rounds like the reference's float64 one.  Otherwise (a few percent of real
-// blocks; every block in "direct" mode) the block is queued and recomputed in
-// exact float64 (explicitly rounded __dadd_rn/__dmul_rn, the reference's
-// operation order) by 8 cooperating threads.
+// in binary32 with the reference's AAN operation order, two lanes per
+// FADD2/FFMA2 instruction: screen_rows (4:2:0) pairs two columns in the
+// column pass and two rows in the row pass, with 2x2 register transposes
+// (explicit PRMT copies) between; screen_cols (4:4:4 / 4:2:2) puts two rows
+// of ONE column transform in a register (aan_col) so the row pass needs no
+// transposes.  A rigorous first-order error bound E = u * sum_i K_i |x_i|
+// (K from tools/analysis/screen_constants.py) brackets each sample; if no
+// rounding boundary of floor(s + 128.5) lies inside [s - E, s + E] for all
+// 64 samples, the binary32 result provably rounds like the reference's
+// float64 one.  Otherwise (a few percent of real blocks; every block in
+// "direct" mode) the block is queued and recomputed in exact float64
+// (explicitly rounded __dadd_rn/__dmul_rn, the reference's operation order)
+// by 8 cooperating threads.
 //
-// Work decomposition: a CTA (64 threads) owns a strip of MCU columns of one
-// image and sweeps down a range of MCU rows.  Step s is two phases:
+// Work decomposition: a CTA (64 threads for 4:4:4 / 4:2:2, 128 for 4:2:0)
+// owns a strip of MCU columns of one image and sweeps down a range of MCU
+// rows.  Step s is two phases:
 //   A. screen: one job (two blocks) per thread - the Y blocks of MCU row s
 //      and the chroma (Cb, Cr) pairs of MCU row s (s+1 for 4:2:0, whose
 //      vertical filter needs the next row) -> sample planes in shared memory;
-//      blocks the screen cannot prove are queued.
+//      blocks the screen cannot prove are queued.  Coefficients arrive as
+//      256-bit L1::no_allocate loads.
 //   B. the queued blocks' exact recompute, overlapped with the pixel stage
 //      of MCU row s-1 (16-pixel items handed out through a shared counter,
 //      so the threads busy with float64 simply take fewer items):
