@@ -527,9 +527,25 @@ __device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefe
 // Unaligned / cropped tail of a 16-pixel RGB row (rare: odd widths, right edge).
 __device__ __noinline__ void store_partial(uint8_t *__restrict__ dst, uint4 a, uint4 b, uint4 c, int nbytes) {
     const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+    // aligned word j of the span starting at dst - m covers item bytes
+    // [4j - m, 4j - m + 4): whole words inside [0, nbytes) as word stores,
+    // the (at most two) cut words byte by byte
+    const int m = (int)(reinterpret_cast<uintptr_t>(dst) & 3);
+    uint32_t *d = reinterpret_cast<uint32_t *>(dst - m);
+    const unsigned sh = 8u * (unsigned)m;
 #pragma unroll
-    for (int i = 0; i < 48; ++i)
-        if (i < nbytes) dst[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+    for (int j = 0; j < 13; ++j) {
+        const int lo = 4 * j - m;
+        if (lo >= nbytes) break;
+        const uint32_t prev = j > 0 ? w[j - 1] : 0u, cur = j < 12 ? w[j] : 0u;
+        const uint32_t v = m ? __funnelshift_l(prev, cur, sh) : cur;
+        if (lo >= 0 && lo + 4 <= nbytes) {
+            d[j] = v;
+        } else {
+            for (int k = 0; k < 4; ++k)
+                if (lo + k >= 0 && lo + k < nbytes) dst[lo + k] = (uint8_t)(v >> (8 * k));
+        }
+    }
 }
 
 // Pixel items are handed out 32 at a time per warp (one shared atomic per
