@@ -47,6 +47,7 @@ WORKLOADS = {
     "1080p420q50": (1920, 1080, 50, "420", 0, 128),
     "1080p444q50": (1920, 1080, 50, "444", 0, 128),
 }
+METRIC = "decoded Mpix/s (parallel phase: dequant+IDCT+upsample+colour)"
 DISTINCT = 8  # distinct synthetic images per rank (replicated to the batch size)
 # "mixed" (BASELINE configs[4], scaled down): a seeded manifest of images of
 # 0.3-24 MP, four aspect ratios, q50-95, all three subsamplings, partitioned
@@ -66,6 +67,8 @@ def parse_args():
     ap.add_argument("--e2e-chunk", type=int, default=4, help="images per pipelined H2D/render/D2H chunk")
     ap.add_argument("--e2e-threads", type=int, default=4, help="host threads calling the render_rows plugin")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-variants", action="store_true",
+                    help="4:4:4/4:2:2: time the shipped/patched/fallback reference builds, 1 and N processes")
     ap.add_argument("--shard", default="images", choices=["images", "rows"],
                     help="N>1: images = each rank its own batch (weak scaling); rows = every rank "
                          "renders its MCU-row range of the SAME images (strong scaling, "
@@ -206,12 +209,32 @@ def ncu_traffic(workload):
         return None
 
 
-def cpu_baseline(images, wl, budget_s=3.0):
-    """Oracle port on the host cores: bounded sample (>= budget_s wall)."""
+def cpu_baseline(images, wl, budget_s=3.0, variants=False):
+    """The reference's CPU path on this host's cores, bounded sample
+    (>= budget_s of CPU work).  4:4:4 / 4:2:2: the reference itself
+    (oracle/_ref, built from /root/reference) in one process per core;
+    4:2:0 (rejected by the reference): the oracle's C restatement on all
+    threads.  variants=True adds BASELINE.md section 3's table: shipped /
+    noexcept-patched native and the numpy fallback, 1 process and N processes."""
     from oracle import oracle
     threads = len(os.sched_getaffinity(0))
     sub = {"444": 0, "422": 1, "420": 2}[wl[3]]
     w, h = wl[0], wl[1]
+    blobs = [b for b, _, _, _ in images[:2]]
+    if wl[3] != "420" and os.path.isdir(os.path.join(REF_DIR, "patched", "hetjpeg")):
+        rate, n_img, wall, _ = reference_render_rate(blobs, wl[3], "patched", threads, budget_s)
+        out = {"value": round(rate, 2), "unit": "Mpix/s", "cores": threads, "kind": "reference",
+               "cpu": cpu_model(), "sample": f"{n_img} x {w}x{h} {wl[3]} images through the reference's "
+               f"render_rows (noexcept-patched native build, oracle/_ref/patched), {threads} processes, "
+               f"{wall:.1f} s"}
+        if variants:
+            tab = {}
+            for v in ("shipped", "patched", "shipped:fallback"):
+                for procs in (1, threads):
+                    r, n, wl_s, _ = reference_render_rate(blobs, wl[3], v, procs, budget_s)
+                    tab[f"{v}/{procs}proc"] = {"mpix_s": round(r, 2), "images": n, "seconds": round(wl_s, 2)}
+            out["variants"] = tab
+        return out
     px = 0
     t0 = time.perf_counter()
     n = 0
@@ -224,8 +247,9 @@ def cpu_baseline(images, wl, budget_s=3.0):
             break
     dt = time.perf_counter() - t0
     return {"value": round(px / dt / 1e6, 2), "unit": "Mpix/s", "cores": threads, "kind": "port",
-            "sample": f"{n} x {w}x{h} {wl[3]} images, {threads} pthreads, {dt:.1f} s wall "
-                      "(oracle/render_oracle.c, float64 AAN as the reference)"}
+            "cpu": cpu_model(), "sample": f"{n} x {w}x{h} {wl[3]} images, {threads} pthreads, {dt:.1f} s wall "
+                      "(oracle/render_oracle.c, the reference's float64 path restated in C; the reference "
+                      "rejects 4:2:0, parser.py:223-229)"}
 
 
 def amdahl_run(images, wl, world, pg, n_images, reserve=0):
@@ -264,45 +288,148 @@ def amdahl_run(images, wl, world, pg, n_images, reserve=0):
                     "stream; medians of 7 interleaved runs, max over ranks"}
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+REF_DIR = os.path.join(ROOT, "oracle", "_ref")
+
+
+def loaded_repo_libs() -> list:
+    """Shared objects from this repository mapped into this process."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for line in fh:
+                path = line.split()[-1] if line.strip() else ""
+                if path.startswith(ROOT) and ".so" in path:
+                    out.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(out)
+
+
+def _ref_proc(variant, blobs, sub, n_img, out_q):
+    """One CPU-baseline process: import the REFERENCE package (oracle/_ref,
+    built from /root/reference by oracle/build_ref.sh), decode with its own
+    parser/entropy stage, then time its render_rows (block_transforms.py:60-75)
+    over n_img images.  Puts (pixels, seconds) on out_q."""
+    kind, _, backend = variant.partition(":")
+    sys.path.insert(0, os.path.join(REF_DIR, kind))
+    if backend == "fallback":
+        os.environ["HETJPEG_BACKEND"] = "fallback"
+    from hetjpeg import block_transforms, entropy, parser, perf_model
+    imgs = []
+    for b in blobs:
+        p = parser.parse_stream(b)
+        c, _ = entropy.decode_all(p, b)
+        imgs.append((c, perf_model._qtable_stack(p), c.geometry))
+    px = block_transforms.alloc_pixels(imgs[0][2].width, imgs[0][2].height)
+    c, qt, g = imgs[0]
+    block_transforms.render_rows(c, qt, px, 0, g.mcu_rows)  # warm-up
+    t0 = time.perf_counter()
+    for i in range(n_img):
+        c, qt, g = imgs[i % len(imgs)]
+        block_transforms.render_rows(c, qt, px, 0, g.mcu_rows)
+    out_q.put((n_img * g.width * g.height, time.perf_counter() - t0))
+
+
+def reference_render_rate(blobs, sub, variant, procs, budget_s):
+    """Mpix/s of the reference's own render_rows, `procs` pinned processes
+    each rendering its own images (the shipped Cython build re-takes the GIL
+    per helper call, so processes, not threads, are the way to use the
+    cores).  Returns (mpix_s, images, seconds)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    # size the per-process sample from a one-image probe
+    q = ctx.Queue()
+    pr = ctx.Process(target=_ref_proc, args=(variant, blobs[:1], sub, 1, q))
+    pr.start()
+    px1, t1 = q.get()
+    pr.join()
+    n_img = max(1, int(budget_s / max(t1, 1e-6)))
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_ref_proc, args=(variant, blobs, sub, n_img, q)) for _ in range(procs)]
+    t0 = time.perf_counter()
+    for p in ps:
+        p.start()
+    res = [q.get() for _ in ps]
+    for p in ps:
+        p.join()
+    wall = max(r[1] for r in res)
+    return sum(r[0] for r in res) / wall / 1e6, n_img * procs, wall, time.perf_counter() - t0
+
+
 def run_reference(args, wl, world, rank, pg):
+    """The reference arm: the reference's CPU implementation of the parallel
+    phase on this box's host cores, same metric / unit / config as ours.
+
+    Nothing from paper_1311_5304_b200 is imported here (no product library
+    in this process).  4:4:4 / 4:2:2: the reference itself (oracle/_ref,
+    noexcept-patched native build = the shipped arithmetic without the Cython-3
+    GIL artefact) through its own parser, entropy stage and render_rows, on
+    all cores as processes.  4:2:0 (the headline): the reference rejects it
+    (parser.py:223-229), so the oracle's plain-C restatement of its float64
+    path (oracle/render_oracle.c) runs on all host threads, coefficients from
+    the oracle's own Huffman restatement (oracle/huffman_oracle.c)."""
     if rank != 0:
         return
-    from paper_1311_5304_b200 import entropy, parser  # host decode only
-    from paper_1311_5304_b200.perf_model import qtable_stack
-    from paper_1311_5304_b200.synth import synth_jpeg
-    from oracle import oracle
+    from oracle import jpeg, oracle
     w, h, q, sub, rst, _ = wl
-    imgs = []
-    for i in range(2):
-        blob = synth_jpeg(w, h, q, sub, seed=i, restart_rows=rst)
-        p = parser.parse_stream(blob)
-        c, _ = entropy.decode_all(p, blob)
-        imgs.append((c, qtable_stack(p)))
+    blobs = [jpeg.synth_jpeg(w, h, q, sub, seed=i, restart_rows=rst) for i in range(2)]
     threads = len(os.sched_getaffinity(0))
     subc = {"444": 0, "422": 1, "420": 2}[sub]
-    # one step = one image over all host threads (bounded sample of the workload)
-    for i in range(args.warmup):
-        c, qt = imgs[i % 2]
-        oracle.render(c.y_blocks, c.cb_blocks, c.cr_blocks, qt, w, h, subc, True, threads)
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        c, qt = imgs[i % 2]
-        oracle.render(c.y_blocks, c.cb_blocks, c.cr_blocks, qt, w, h, subc, True, threads)
-    dt = time.perf_counter() - t0
-    value = args.steps * w * h / dt / 1e6
+    use_ref = sub != "420" and os.path.isdir(os.path.join(REF_DIR, "patched", "hetjpeg"))
+    budget = 4.0  # seconds of CPU work in the timed region (bounded sample)
+    if use_ref:
+        # warm-up and timed region are sized in images; steps = equal slices
+        rate, n_img, wall, _ = reference_render_rate(blobs, sub, "patched", threads, budget)
+        dt = n_img * w * h / rate / 1e6
+        kind, how = "reference", (f"reference render_rows (oracle/_ref/patched: _native.pyx built with "
+                                  f"noexcept, shipped arithmetic) in {threads} processes, "
+                                  f"{n_img} x {w}x{h} {sub} images, {wall:.1f} s")
+        per_step = n_img / max(args.steps, 1)
+    else:
+        imgs = []
+        for b in blobs:
+            d = jpeg.decode(b)
+            imgs.append((d.y, d.cb, d.cr, d.q))
+        t_probe = time.perf_counter()
+        oracle.render(*imgs[0], w, h, subc, True, threads)
+        t_probe = time.perf_counter() - t_probe
+        per_step = max(1, int(round(budget / max(args.steps, 1) / max(t_probe, 1e-6))))
+        for i in range(args.warmup):
+            oracle.render(*imgs[i % 2], w, h, subc, True, threads)
+        t0 = time.perf_counter()
+        n_img = 0
+        for s in range(args.steps):
+            for k in range(per_step):
+                oracle.render(*imgs[n_img % 2], w, h, subc, True, threads)
+                n_img += 1
+        dt = time.perf_counter() - t0
+        rate = n_img * w * h / dt / 1e6
+        kind, how = "port", (f"{per_step} image(s) per step, {n_img} x {w}x{h} {sub} images, {threads} "
+                             "pthreads, oracle/render_oracle.c (the reference's float64 path restated in C; "
+                             "the reference rejects 4:2:0, parser.py:223-229)")
     line = {
-        "impl": "reference", "metric": "decoded Mpix/s (parallel phase)", "value": round(value, 2),
+        "impl": "reference", "metric": METRIC, "value": round(rate, 2),
         "unit": "Mpix/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(dt / args.steps * 1e3, 4), "higher_is_better": True,
-        "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{w}x{h} {sub} q{q}", "images_per_step": 1},
-        "cpu_baseline": {"value": round(value, 2), "unit": "Mpix/s", "cores": threads,
-                         "kind": "port",
-                         "sample": f"1 image per step, {threads} pthreads; the reference rejects "
-                                   "4:2:0 (parser.py:223-229), so its float64 path is timed "
-                                   "through the bit-exact C restatement oracle/render_oracle.c"},
-        "e2e": {"value": round(value, 2), "unit": "Mpix/s", "h2d_bytes_per_step": 0,
+        "ms_per_step": round(dt / max(args.steps, 1) * 1e3, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{w}x{h} {sub} q{q}" + (" rst" if rst else ""),
+                   "images_per_step": round(per_step, 3), "host": cpu_model()},
+        "cpu_baseline": {"value": round(rate, 2), "unit": "Mpix/s", "cores": threads, "kind": kind,
+                         "sample": how, "cpu": cpu_model()},
+        "e2e": {"value": round(rate, 2), "unit": "Mpix/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "repo_libs_loaded": loaded_repo_libs(),
     }
     print(json.dumps(line), flush=True)
 
@@ -400,7 +527,7 @@ def run_mixed(args, world, rank, local, pg):
     db.close()
     if rank == 0:
         line = {
-            "metric": "decoded Mpix/s (parallel phase: dequant+IDCT+upsample+colour)",
+            "metric": METRIC,
             "value": round(value, 1), "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -421,8 +548,22 @@ def run_mixed(args, world, rank, local, pg):
         pg.destroy_process_group()
 
 
+def spawn_ranks(args):
+    """`--gpus N` without a launcher: re-exec under torch.distributed.run with
+    N local ranks (one process per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
     if args.workload == "mixed":
         world, rank, local, pg = dist_setup()
         if args.impl == "reference":
@@ -599,11 +740,11 @@ def main():
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(images, wl)
+        cpu = cpu_baseline(images, wl, variants=args.cpu_variants)
 
     if rank == 0:
         line = {
-            "metric": "decoded Mpix/s (parallel phase: dequant+IDCT+upsample+colour)",
+            "metric": METRIC,
             "value": round(value, 1), "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5),
             "higher_is_better": True, "scaling": "strong" if rows_mode else "weak", "vs_baseline": None,
