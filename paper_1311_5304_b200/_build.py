@@ -4,7 +4,9 @@
     python -m paper_1311_5304_b200._build --all    # + the CPU oracle (tests only)
 
 Output: paper_1311_5304_b200/libhetjpeg_b200.so (git-ignored, travels with
-gpurun snapshots).  Rebuilds only when a source is newer than the library.
+gpurun snapshots).  Rebuilds whenever the SHA-256 of the sources, headers,
+flags and nvcc version differs from the one recorded next to the library
+(libhetjpeg_b200.so.sha256), so a stale prebuilt binary is never reused.
 """
 from __future__ import annotations
 
@@ -16,20 +18,38 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhetjpeg_b200.so")
-SOURCES = ["hj_render.cu", "hj_blockops.cu", "hj_api.cu", "hj_entropy.cpp", "hj_entropy_fast.cpp"]
-HEADERS = ["hj_render.cuh", "hj_common.cuh", "hj_screen.h", "hj_tables.h", os.path.join("..", "..", "include", "hetjpeg_b200.h")]
+SOURCES = ["hj_render.cu", "hj_blockops.cu", "hj_api.cu", "hj_huffman.cpp"]
+HEADERS = ["hj_render.cuh", "hj_common.cuh", "hj_screen.h", "hj_tables.h", "hj_huffman.h", "hj_error.h",
+           os.path.join("..", "..", "include", "hetjpeg_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
          "-Xptxas", "-warn-spills"]
 
 
+def source_hash() -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for name in SOURCES + HEADERS:
+        h.update(name.encode())
+        with open(os.path.join(CSRC, name), "rb") as fh:
+            h.update(fh.read())
+    h.update(" ".join(ARCH + FLAGS).encode())
+    try:
+        h.update(subprocess.run([NVCC, "--version"], capture_output=True, text=True).stdout.encode())
+    except OSError:
+        pass
+    return h.hexdigest()
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
-    return any(os.path.getmtime(d) > t for d in deps)
+    try:
+        with open(LIB + ".sha256") as fh:
+            return fh.read().strip() != source_hash()
+    except OSError:
+        return True
 
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
@@ -42,6 +62,8 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
     os.replace(LIB + ".tmp", LIB)
+    with open(LIB + ".sha256", "w") as fh:
+        fh.write(source_hash() + "\n")
     return LIB
 
 

@@ -17,6 +17,7 @@
 
 #include <cuda_runtime.h>
 
+#include "hj_error.h"
 #include "hj_render.cuh"
 
 // tile-planner model parameters (choose_rows_per_tile)
@@ -36,14 +37,18 @@
 
 
 namespace {
-
 thread_local std::string t_error;
-std::atomic<uint64_t> g_launches{0};
+}  // namespace
 
-hj_status fail(hj_status code, const std::string &msg) {
+hj_status hj::fail(hj_status code, const std::string &msg) {
     t_error = msg;
     return code;
 }
+
+namespace {
+
+using hj::fail;
+std::atomic<uint64_t> g_launches{0};
 
 hj_status cuda_fail(cudaError_t e, const char *what) {
     return fail(HJ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -243,17 +248,34 @@ hj_status plan_launch(const Plan *p, cudaStream_t stream) {
         }
     }
     if (ng > 1) HJ_CUDA(cudaEventRecord(p->ev[0], stream));
-    for (size_t k = 0; k < ng; ++k) {
+    // every forked group that was queued is joined back into `stream`, also
+    // when a later launch fails, so the caller's stream order stays complete
+    hj_status st_out = HJ_OK;
+    size_t joined = 1;
+    for (size_t k = 0; k < ng && st_out == HJ_OK; ++k) {
         const auto &g = p->groups[k];
         cudaStream_t st = k == 0 ? stream : p->side[k - 1];
-        if (k > 0) HJ_CUDA(cudaStreamWaitEvent(st, p->ev[0], 0));
-        cudaError_t e = hj::launch_render(g.sub, g.direct, imgs, tiles + g.offset, g.count, st);
-        if (e != cudaSuccess) return cuda_fail(e, "render kernel launch");
+        cudaError_t e = k > 0 ? cudaStreamWaitEvent(st, p->ev[0], 0) : cudaSuccess;
+        if (e == cudaSuccess) e = hj::launch_render(g.sub, g.direct, imgs, tiles + g.offset, g.count, st);
+        if (e != cudaSuccess) {
+            st_out = cuda_fail(e, "render kernel launch");
+            break;
+        }
         g_launches.fetch_add(1, std::memory_order_relaxed);
-        if (k > 0) HJ_CUDA(cudaEventRecord(p->ev[k], st));
+        if (k > 0) {
+            e = cudaEventRecord(p->ev[k], st);
+            if (e != cudaSuccess) {
+                st_out = cuda_fail(e, "cudaEventRecord(join)");
+                break;
+            }
+            joined = k + 1;
+        }
     }
-    for (size_t k = 1; k < ng; ++k) HJ_CUDA(cudaStreamWaitEvent(stream, p->ev[k], 0));
-    return HJ_OK;
+    for (size_t k = 1; k < joined; ++k) {
+        cudaError_t e = cudaStreamWaitEvent(stream, p->ev[k], 0);
+        if (e != cudaSuccess && st_out == HJ_OK) st_out = cuda_fail(e, "cudaStreamWaitEvent(join)");
+    }
+    return st_out;
 }
 
 // Per-thread context of the synchronous drop-in API.
@@ -488,17 +510,23 @@ static bool pipe_use_submitter() {
 
 static hj_status pipe_run(const hj_pipe_image_t *images, int32_t n_images, int32_t n_threads,
                           void *const *streams, int gpu) {
-    if (n_images < 0 || (n_images > 0 && !images) || n_threads < 1 || (gpu && !streams)) return HJ_ERR_ARG;
+    if (n_images < 0 || (n_images > 0 && !images) || n_threads < 1 || (gpu && !streams))
+        return fail(HJ_ERR_ARG, "pipeline: bad image array, thread count or stream array");
     if (n_images == 0) return HJ_OK;
     int device = 0;
-    if (gpu && cudaGetDevice(&device) != cudaSuccess) return HJ_ERR_CUDA;
+    if (gpu) HJ_CUDA(cudaGetDevice(&device));
     const bool submitter = gpu && pipe_use_submitter();
     std::atomic<int> next{0};
     std::atomic<int> first_err{HJ_OK};
+    std::mutex err_mu;
+    std::string err_msg;  // hj_last_error is per thread: carry the first one to the caller
     auto record = [&](hj_status s) {
         if (s != HJ_OK) {
             int expect = HJ_OK;
-            first_err.compare_exchange_strong(expect, (int)s);
+            if (first_err.compare_exchange_strong(expect, (int)s)) {
+                std::lock_guard<std::mutex> g(err_mu);
+                err_msg = t_error;
+            }
         }
     };
     std::mutex mu;
@@ -551,7 +579,8 @@ static hj_status pipe_run(const hj_pipe_image_t *images, int32_t n_images, int32
             if (e != cudaSuccess && first_err.load() == HJ_OK) return cuda_fail(e, "pipeline sync");
         }
     }
-    return (hj_status)first_err.load();
+    if (first_err.load() != HJ_OK) return fail((hj_status)first_err.load(), "pipeline: " + err_msg);
+    return HJ_OK;
 }
 
 hj_status hj_pipeline_run(const hj_pipe_image_t *images, int32_t n_images, int32_t n_threads,

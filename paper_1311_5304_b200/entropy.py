@@ -5,7 +5,7 @@ API of the reference's `hetjpeg.entropy` (pkg/src/hetjpeg/entropy.py):
 `dezigzag`, `CoefficientBuffer`, `alloc_coefficients`, `EntropyCursor`,
 `new_cursor`, `decode_rows`, `decode_all`, with the same int64[8] cursor
 state layout.  Decoding runs in the native C++ decoder
-(`hj_decode_mcu_rows`, csrc/hj_entropy.cpp) with the GIL released (ctypes),
+(`hj_decode_mcu_rows`, csrc/hj_huffman.cpp) with the GIL released (ctypes),
 so several host threads decode different images truly in parallel - the
 reference's Cython decoder re-takes the GIL per helper call.
 
