@@ -118,9 +118,9 @@ def upsample_row_422(row, left=None, right=None):
     _lib.require_device()
     rows = np.asarray(row)
     single = rows.ndim == 1
-    rows = rows.reshape(-1, 8) if rows.size % 8 == 0 and rows.size else rows
-    if rows.ndim != 2 or rows.shape[1] != 8:
+    if rows.shape not in ((8,),) and not (rows.ndim == 2 and rows.shape[1] == 8):
         raise ValueError("expected an 8-sample chroma row")
+    rows = rows.reshape(-1, 8)
     n = len(rows)
 
     def nb(v):
@@ -138,13 +138,21 @@ def upsample_row_422(row, left=None, right=None):
 
 def ycbcr_to_rgb(y, cb, cr):
     """Colour conversion (fallback.py:142-150): scalars or arrays of samples
-    in [0, 255] -> (r, g, b) uint8 arrays of the broadcast shape."""
+    -> (r, g, b) uint8 arrays of the broadcast shape.  The exact integer
+    conversion (proven over all 2^24 inputs) covers what a decoder produces:
+    integer-valued samples in [0, 255], of any numeric dtype.  Other values
+    (fractional or out of range), which the reference would convert in
+    float64, are rejected rather than truncated."""
     _lib.require_device()
     yb, cbb, crb = np.broadcast_arrays(np.asarray(y), np.asarray(cb), np.asarray(cr))
     shape = yb.shape
     for a in (yb, cbb, crb):
+        if a.dtype.kind not in "biuf":
+            raise TypeError(f"samples must be numeric, got {a.dtype}")
         if a.size and (a.min() < 0 or a.max() > 255):
             raise ValueError("samples must lie in [0, 255]")
+        if a.dtype.kind == "f" and a.size and not np.array_equal(a, np.floor(a)):
+            raise ValueError("samples must be integer-valued (the exact conversion is defined on 8-bit samples)")
     flat = [np.ascontiguousarray(a, dtype=np.uint8).reshape(-1) for a in (yb, cbb, crb)]
     n = flat[0].size
     rgb = np.empty((n, 3), np.uint8)

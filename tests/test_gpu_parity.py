@@ -2,6 +2,7 @@
 the reference's own render_rows output for 4:4:4/4:2:2) and with the CPU
 oracle (4:2:0 extension, full BASELINE sizes, adversarial inputs).
 Bar: bit-exact RGB.  Calls go through the C ABI (ctypes)."""
+import os
 import threading
 
 import numpy as np
@@ -282,3 +283,57 @@ def test_strip_widths_sweep(cuda, sub):
             want = oracle.render(c.y_blocks, c.cb_blocks, c.cr_blocks, q, g.width, g.height, code, True)
             assert np.array_equal(out, want), (sub, g.width)
         batch.close()
+
+
+def _single_ops():
+    return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "single_ops.npz"))
+
+
+def test_single_mcu_forms_match_reference_vectors(cuda):
+    """upsample_row_422 / fused_upsample_color_422 / fused_idct_color_444
+    against the reference's own outputs (tests/golden/make_single_ops.py),
+    including the float64 G tie pair (Cb, Cr) = (78, 178)."""
+    from paper_1311_5304_b200 import block_transforms as bt
+    z = _single_ops()
+    nb = lambda v: None if v < 0 else int(v)  # noqa: E731
+    for r, a, b, want in zip(z["up_rows"], z["up_left"], z["up_right"], z["up_out"]):
+        assert bt.upsample_row_422(r, nb(a), nb(b)).tolist() == want.tolist()
+    for y, cb, cr, k, want in zip(z["f422_y"], z["f422_cb"], z["f422_cr"], z["f422_nb"], z["f422_out"]):
+        got = bt.fused_upsample_color_422(y, cb, cr, *[nb(v) for v in k])
+        assert np.array_equal(got, want)
+    for blk, q, wf, wd in zip(z["f444_blocks"], z["f444_q"], z["f444_fast"], z["f444_direct"]):
+        assert np.array_equal(bt.fused_idct_color_444(*blk, *q, fast=True), wf)
+        assert np.array_equal(bt.fused_idct_color_444(*blk, *q, fast=False), wd)
+
+
+def _h2v2_pin_cases():
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "h2v2_pin.npz"))
+    return [(k[:-5], bytes(z[k]), z[k[:-5] + "_rgb"]) for k in z.files if k.endswith("_jpeg")]
+
+
+@pytest.mark.parametrize("case", _h2v2_pin_cases(), ids=lambda c: c[0])
+def test_render_420_pinned_to_libjpeg_turbo(cuda, case):
+    """The 4:2:0 render kernel against libjpeg-turbo's h2v2 fancy upsampler
+    (DC-only 16-aligned images, tests/golden/make_h2v2_pin.py), through the
+    drop-in render_rows and through a device batch."""
+    from paper_1311_5304_b200 import device, entropy, parser
+    from paper_1311_5304_b200.block_transforms import alloc_pixels, render_rows
+    from paper_1311_5304_b200.perf_model import qtable_stack
+    name, blob, want = case
+    p = parser.parse_stream(blob)
+    c, _ = entropy.decode_all(p, blob)
+    q = qtable_stack(p)
+    px = alloc_pixels(p.width, p.height)
+    render_rows(c, q, px, 0, c.geometry.mcu_rows)
+    assert np.array_equal(px.data, want)
+    db = device.DeviceBatch([c.geometry, c.geometry])
+    st = device.Stream()
+    for i in range(2):
+        db.upload_coefficients(i, c, st)
+        db.upload_qtables(i, q, st)
+    db.render(stream=st)
+    out = np.zeros_like(want)
+    db.download_rgb(1, out, st)
+    st.synchronize()
+    db.close()
+    assert np.array_equal(out, want)

@@ -135,3 +135,25 @@ def test_cursor_state_is_chunking_invariant():
             row += n
             assert st.tolist() == c["states"][row - 1], (c["base"], c["ops"], row)
         assert _sha(y, cb, cr) == c["sha256"]
+
+
+def _dc_wrap_cases():
+    z = np.load(os.path.join(HERE, "golden", "dc_wrap.npz"))
+    return [(k[:-5], bytes(z[k]), z[k[:-5] + "_y"], z[k[:-5] + "_cb"], z[k[:-5] + "_cr"])
+            for k in z.files if k.endswith("_jpeg")]
+
+
+@pytest.mark.parametrize("case", _dc_wrap_cases(), ids=lambda c: c[0])
+@pytest.mark.parametrize("threads", [1, 3])
+def test_dc_predictor_wraps_like_the_reference(case, threads):
+    """DC predictors run far past int16 (crafted scans, tests/golden/
+    make_dc_wrap.py): accumulate in 64 bits, wrap on store
+    (_native.pyx:162-163) - the cursor and the whole-scan decoder."""
+    name, blob, y, cb, cr = case
+    p = parser.parse_stream(blob)
+    c, cur = entropy.decode_all(p, blob)
+    assert np.array_equal(c.y_blocks, y) and np.array_equal(c.cb_blocks, cb) and np.array_equal(c.cr_blocks, cr)
+    assert max(abs(v) for v in cur.dc_predictors) < 2 ** 40
+    fs = entropy.FastScan(p)
+    out = fs.decode(blob, threads=threads)
+    assert np.array_equal(out.y_blocks, y) and np.array_equal(out.cb_blocks, cb) and np.array_equal(out.cr_blocks, cr)

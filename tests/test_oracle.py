@@ -1,6 +1,8 @@
 """The CPU oracle against the reference's own outputs (golden fixtures made
 by tests/golden/make_golden.py from /root/reference) and the SPEC.md
 known-answer vectors.  CPU only."""
+import os
+
 import numpy as np
 import pytest
 
@@ -59,3 +61,43 @@ def test_spec_vectors():
     # SPEC.md:199-201 colour conversion
     out = oracle.ycbcr_to_rgb([128, 76, 255], [128, 85, 128], [128, 255, 128])
     assert out.tolist() == [[128, 128, 128], [254, 0, 0], [255, 255, 255]]
+
+
+def test_oracle_single_mcu_forms_match_reference_vectors():
+    """The oracle's render / colour on the reference's single-MCU vectors
+    (tests/golden/single_ops.npz, from fallback.py:122-180)."""
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "single_ops.npz"))
+    for blk, q, wf, wd in zip(z["f444_blocks"][:60], z["f444_q"][:60], z["f444_fast"][:60], z["f444_direct"][:60]):
+        for fast, want in ((True, wf), (False, wd)):
+            got = oracle.render(blk[0:1], blk[1:2], blk[2:3], q, 8, 8, 0, fast)
+            assert np.array_equal(got.reshape(64, 3), want)
+    # colour of the reference-upsampled rows = the reference's fused 4:2:2 rows
+    up = lambda r, a, b: [(int(r[0]) if a < 0 else (3 * int(r[0]) + int(a) + 1) // 4)] + [  # noqa: E731
+        v for k in range(8) for v in ((3 * int(r[k]) + int(r[k - 1]) + 1) // 4 if k else None,
+                                      (3 * int(r[k]) + int(r[k + 1]) + 2) // 4 if k < 7 else None)
+        if v is not None] + [int(r[7]) if b < 0 else (3 * int(r[7]) + int(b) + 2) // 4]
+    for r, a, b, want in zip(z["up_rows"], z["up_left"], z["up_right"], z["up_out"]):
+        assert up(r, a, b) == want.tolist()
+    for y, cb, cr, k, want in zip(z["f422_y"], z["f422_cb"], z["f422_cr"], z["f422_nb"], z["f422_out"]):
+        got = oracle.ycbcr_to_rgb(y, up(cb, k[0], k[1]), up(cr, k[2], k[3]))
+        assert np.array_equal(np.asarray(got).reshape(16, 3), want)
+
+
+def _h2v2_pin_cases():
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "h2v2_pin.npz"))
+    return [(k[:-5], bytes(z[k]), z[k[:-5] + "_rgb"]) for k in z.files if k.endswith("_jpeg")]
+
+
+@pytest.mark.parametrize("case", _h2v2_pin_cases(), ids=lambda c: c[0])
+def test_oracle_420_upsampler_pinned_to_libjpeg_turbo(case):
+    """4:2:0 extension vs libjpeg-turbo's h2v2_fancy_upsample on DC-only
+    16-aligned images (tests/golden/make_h2v2_pin.py): the RGB the reference
+    would produce from libjpeg-turbo's upsampled planes."""
+    from paper_1311_5304_b200 import entropy, parser
+    from paper_1311_5304_b200.perf_model import qtable_stack
+    name, blob, want = case
+    p = parser.parse_stream(blob)
+    c, _ = entropy.decode_all(p, blob)
+    assert not any(np.count_nonzero(b[:, 1:]) for b in (c.y_blocks, c.cb_blocks, c.cr_blocks))  # DC-only
+    got = oracle.render(c.y_blocks, c.cb_blocks, c.cr_blocks, qtable_stack(p), p.width, p.height, 2)
+    assert np.array_equal(got, want)
