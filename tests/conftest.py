@@ -50,3 +50,26 @@ def has_gpu() -> bool:
         return _lib.lib.hj_device_count() > 0
     except Exception:
         return False
+
+
+class IslowCase:
+    """One libjpeg-turbo golden of the islow mode (tests/golden/make_islow_golden.py)."""
+
+    def __init__(self, name, jpeg, sha):
+        self.name, self.jpeg, self.sha = name, jpeg, sha
+
+    def __repr__(self):
+        return self.name
+
+
+def islow_cases():
+    z = np.load(os.path.join(GOLDEN, "islow_golden.npz"))
+    return [IslowCase(k[:-5], bytes(z[k]), str(z[k[:-5] + "_sha"])) for k in sorted(z.files) if k.endswith("_jpeg")]
+
+
+ISLOW_CASES = islow_cases()
+
+
+def rgb_sha(rgb) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(rgb).tobytes()).hexdigest()

@@ -101,3 +101,32 @@ def test_oracle_420_upsampler_pinned_to_libjpeg_turbo(case):
     assert not any(np.count_nonzero(b[:, 1:]) for b in (c.y_blocks, c.cb_blocks, c.cr_blocks))  # DC-only
     got = oracle.render(c.y_blocks, c.cb_blocks, c.cr_blocks, qtable_stack(p), p.width, p.height, 2)
     assert np.array_equal(got, want)
+
+
+from conftest import ISLOW_CASES, rgb_sha  # noqa: E402
+
+
+@pytest.mark.parametrize("case", ISLOW_CASES, ids=repr)
+def test_islow_oracle_matches_libjpeg_turbo(case):
+    """The islow-mode oracle (libjpeg_oracle.c) reproduces libjpeg-turbo's
+    decode of the same JPEG (tests/golden/make_islow_golden.py)."""
+    from paper_1311_5304_b200 import entropy, parser
+    from paper_1311_5304_b200.perf_model import qtable_stack
+    p = parser.parse_stream(case.jpeg)
+    c, _ = entropy.decode_all(p, case.jpeg)
+    sub = {8: 0}.get(c.geometry.mcu_width, 1 if c.geometry.mcu_height == 8 else 2)
+    got = oracle.render_islow(c.y_blocks, c.cb_blocks, c.cr_blocks, qtable_stack(p), p.width, p.height, sub)
+    assert rgb_sha(got) == case.sha
+
+
+def test_islow_oracle_row_ranges_compose():
+    from paper_1311_5304_b200 import entropy, parser
+    from paper_1311_5304_b200.perf_model import qtable_stack
+    case = [c for c in ISLOW_CASES if "160x96_420" in c.name][0]
+    p = parser.parse_stream(case.jpeg)
+    c, _ = entropy.decode_all(p, case.jpeg)
+    q = qtable_stack(p)
+    rgb = np.zeros((p.height, p.width, 3), np.uint8)
+    for r0 in range(c.geometry.mcu_rows):
+        oracle.render_islow(c.y_blocks, c.cb_blocks, c.cr_blocks, q, p.width, p.height, 2, r0, 1, rgb)
+    assert rgb_sha(rgb) == case.sha
