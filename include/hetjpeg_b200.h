@@ -42,7 +42,15 @@ typedef enum {
 enum { HJ_SUB_444 = 0, HJ_SUB_422 = 1, HJ_SUB_420 = 2 };
 
 /* Flags for hj_image_t.flags */
-enum { HJ_FLAG_DIRECT_IDCT = 1 };   /* idct="direct" (cli.py:249); default AAN "fast" */
+enum {
+    HJ_FLAG_DIRECT_IDCT = 1,  /* idct="direct" (cli.py:249); default AAN "fast" */
+    HJ_FLAG_ISLOW_IDCT = 2    /* idct="islow": libjpeg's integer decode (jidctint islow IDCT,
+                                 jdsample fancy upsampling with real-size edges, jdcolor
+                                 colour) - north_star's fixed-point mode; not the
+                                 reference's float64 arithmetic */
+};
+/* The `fast` argument of hj_render_rows: the IDCT path. */
+enum { HJ_IDCT_DIRECT = 0, HJ_IDCT_FAST = 1, HJ_IDCT_ISLOW = 2 };
 
 /* One image (or an MCU-row range of one) for the device-resident batch API.
  * All pointers are DEVICE pointers.  Layout of the coefficient planes is the
@@ -119,7 +127,8 @@ uint64_t hj_exact_block_count(void);
  * (kernels/_native.pyx:532-549, kernels/fallback.py:224-260): HOST arrays,
  * blocks of the whole image, rgb (height, width, 3) written in place for the
  * MCU rows [row0, row0+n_rows); returns after the RGB rows are in `rgb`.
- * `fast` selects the AAN (1) or direct-basis (0) transform; `fused` is
+ * `fast` selects the AAN (1) or direct-basis (0) transform of the
+ * reference, or HJ_IDCT_ISLOW (2) for libjpeg's islow decode; `fused` is
  * accepted for interface parity and never changes bytes.  y/cb/cr must hold
  * every block of the image (n_y_blocks / n_c_blocks give their counts, used
  * for bounds checks).  Re-entrant: each host thread uses its own stream and

@@ -30,6 +30,25 @@ HJ_ERR_NODEVICE = 19
 
 SUB_444, SUB_422, SUB_420 = 0, 1, 2
 FLAG_DIRECT_IDCT = 1
+FLAG_ISLOW_IDCT = 2
+IDCT_DIRECT, IDCT_FAST, IDCT_ISLOW = 0, 1, 2
+
+
+def idct_code(fast) -> int:
+    """The IDCT path of a `fast` argument: True = the reference's AAN, False =
+    its direct basis (both float64, kernels/_native.pyx:364-388), "islow" =
+    libjpeg's integer decode (north_star's jidctint mode; HJ_IDCT_ISLOW)."""
+    if isinstance(fast, str):
+        if fast == "islow":
+            return IDCT_ISLOW
+        if fast in ("fast", "direct"):
+            return IDCT_FAST if fast == "fast" else IDCT_DIRECT
+        raise ValueError(f"unknown idct path {fast!r}")
+    return IDCT_FAST if fast else IDCT_DIRECT
+
+
+def image_flags(fast) -> int:
+    return {IDCT_FAST: 0, IDCT_DIRECT: FLAG_DIRECT_IDCT, IDCT_ISLOW: FLAG_ISLOW_IDCT}[idct_code(fast)]
 
 
 class CudaError(HetJpegError, RuntimeError):

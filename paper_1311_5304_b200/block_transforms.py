@@ -44,7 +44,7 @@ def alloc_pixels(width: int, height: int, pinned: bool = False) -> PixelBuffer:
 
 
 def render_rows(coeffs, qtables, pixels: PixelBuffer, row0: int, n_rows: int,
-                fast: bool = True, fused: bool = True, backend=None) -> None:
+                fast=True, fused: bool = True, backend=None) -> None:
     """Parallel phase over MCU rows [row0, row0 + n_rows) (block_transforms.py:60-75).
 
     Dispatches on the MCU shape: 8x8 -> 4:4:4, 16x8 -> 4:2:2, 16x16 -> 4:2:0.

@@ -76,6 +76,9 @@ hj_status validate(const hj_image_t &im) {
     if (im.row0 < 0 || im.n_rows < 0 || im.row0 + im.n_rows > im.mcu_rows)
         return fail(HJ_ERR_ARG, "MCU row range outside the image");
     if (!im.y || !im.cb || !im.cr || !im.q || !im.rgb) return fail(HJ_ERR_ARG, "null pointer");
+    if ((im.flags & ~(HJ_FLAG_DIRECT_IDCT | HJ_FLAG_ISLOW_IDCT)) != 0 ||
+        (im.flags & (HJ_FLAG_DIRECT_IDCT | HJ_FLAG_ISLOW_IDCT)) == (HJ_FLAG_DIRECT_IDCT | HJ_FLAG_ISLOW_IDCT))
+        return fail(HJ_ERR_ARG, "flags: unknown bits or both direct and islow");
     return HJ_OK;
 }
 
@@ -87,7 +90,8 @@ struct Plan {
     size_t bytes = 0;
     size_t tile_base = 0;  // byte offset of the Tile array in dev
     int n_images = 0;
-    struct Group { int sub; bool direct; int offset; int count; };
+    // kind: 0 AAN, 1 direct basis (both the reference's float64 mode), 2 islow
+    struct Group { int sub; int kind; int offset; int count; };
     std::vector<Group> groups;
     // a batch mixing subsamplings launches one kernel per family; they are
     // independent, so they run concurrently on forked streams
@@ -117,7 +121,13 @@ static int64_t strips_of(int mpr, int S, int sub) {
     return (mpr + S - 1) / S;
 }
 
-int choose_rows_per_tile(const hj_image_t *images, int n, int sub, int direct, int S, int64_t slots) {
+// Launch group of an image: the float64 AAN (0) / direct (1) paths share a
+// kernel but keep separate tiles (their costs differ); islow (2) has its own.
+static int idct_kind(const hj_image_t &im) {
+    return (im.flags & HJ_FLAG_ISLOW_IDCT) ? 2 : (im.flags & HJ_FLAG_DIRECT_IDCT) ? 1 : 0;
+}
+
+int choose_rows_per_tile(const hj_image_t *images, int n, int sub, int kind, int S, int64_t slots) {
     const double overhead = sub == HJ_SUB_420 ? HJ_PLAN_OVH_420 : HJ_PLAN_OVH;  // in steps
     const int64_t min_waves = sub == HJ_SUB_420 ? HJ_PLAN_MINW_420 : HJ_PLAN_MINW;
     int best_T = 8;
@@ -126,7 +136,7 @@ int choose_rows_per_tile(const hj_image_t *images, int n, int sub, int direct, i
         int64_t tiles = 0;
         for (int i = 0; i < n; ++i) {
             const hj_image_t &im = images[i];
-            if (im.subsampling != sub || ((im.flags & HJ_FLAG_DIRECT_IDCT) != 0) != (direct != 0)) continue;
+            if (im.subsampling != sub || idct_kind(im) != kind) continue;
             tiles += strips_of(im.mcus_per_row, S, sub) * ((im.n_rows + T - 1) / T);
         }
         if (tiles == 0) return best_T;
@@ -148,14 +158,14 @@ void build_tiles(const hj_image_t *images, int n, std::vector<hj::Tile> &tiles,
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     for (int sub = HJ_SUB_444; sub <= HJ_SUB_420; ++sub) {
         const int64_t slots = (int64_t)sms * hj::ctas_per_sm(sub);  // resident CTAs
-        for (int direct = 0; direct < 2; ++direct) {
+        for (int kind = 0; kind < 3; ++kind) {
             int S = hj::strip_width(sub);
             int64_t strip_rows = 0, strips = 0;
             for (;;) {
                 strip_rows = strips = 0;
                 for (int i = 0; i < n; ++i) {
                     const hj_image_t &im = images[i];
-                    if (im.subsampling != sub || ((im.flags & HJ_FLAG_DIRECT_IDCT) != 0) != (direct != 0)) continue;
+                    if (im.subsampling != sub || idct_kind(im) != kind) continue;
                     const int64_t ns = strips_of(im.mcus_per_row, S, sub);
                     strips += ns;
                     strip_rows += ns * im.n_rows;
@@ -165,11 +175,11 @@ void build_tiles(const hj_image_t *images, int n, std::vector<hj::Tile> &tiles,
                 S = (S + 1) / 2;
             }
             if (strip_rows == 0) continue;
-            const int T = choose_rows_per_tile(images, n, sub, direct, S, slots);
-            Plan::Group g{sub, direct != 0, (int)tiles.size(), 0};
+            const int T = choose_rows_per_tile(images, n, sub, kind, S, slots);
+            Plan::Group g{sub, kind, (int)tiles.size(), 0};
             for (int i = 0; i < n; ++i) {
                 const hj_image_t &im = images[i];
-                if (im.subsampling != sub || ((im.flags & HJ_FLAG_DIRECT_IDCT) != 0) != (direct != 0)) continue;
+                if (im.subsampling != sub || idct_kind(im) != kind) continue;
                 const int ns = (int)strips_of(im.mcus_per_row, S, sub);
                 for (int r = im.row0; r < im.row0 + im.n_rows; r += T) {
                     int r1 = std::min(im.row0 + im.n_rows, r + T);
@@ -256,7 +266,7 @@ hj_status plan_launch(const Plan *p, cudaStream_t stream) {
         const auto &g = p->groups[k];
         cudaStream_t st = k == 0 ? stream : p->side[k - 1];
         cudaError_t e = k > 0 ? cudaStreamWaitEvent(st, p->ev[0], 0) : cudaSuccess;
-        if (e == cudaSuccess) e = hj::launch_render(g.sub, g.direct, imgs, tiles + g.offset, g.count, st);
+        if (e == cudaSuccess) e = hj::launch_render(g.sub, g.kind == 2 ? hj::kModeIslow : hj::kModeRef, imgs, tiles + g.offset, g.count, st);
         if (e != cudaSuccess) {
             st_out = cuda_fail(e, "render kernel launch");
             break;
@@ -610,7 +620,7 @@ static hj_status render_rows_impl(const int16_t *y, const int16_t *cb, const int
     im.row0 = row0;
     im.n_rows = n_rows;
     im.subsampling = subsampling;
-    im.flags = fast ? 0 : HJ_FLAG_DIRECT_IDCT;
+    im.flags = fast == HJ_IDCT_ISLOW ? HJ_FLAG_ISLOW_IDCT : fast ? 0 : HJ_FLAG_DIRECT_IDCT;
     im.y = im.cb = im.cr = reinterpret_cast<const int16_t *>(16);  // placeholders for validate
     im.q = reinterpret_cast<const int32_t *>(16);
     im.rgb = reinterpret_cast<uint8_t *>(16);
@@ -670,7 +680,7 @@ static hj_status render_rows_impl(const int16_t *y, const int16_t *cb, const int
     const hj_image_t *dimg = reinterpret_cast<const hj_image_t *>(misc + img_off);
     const hj::Tile *dtiles = reinterpret_cast<const hj::Tile *>(misc + tile_off);
     for (const auto &g : groups) {
-        cudaError_t e = hj::launch_render(g.sub, g.direct, dimg, dtiles + g.offset, g.count, c->stream);
+        cudaError_t e = hj::launch_render(g.sub, g.kind == 2 ? hj::kModeIslow : hj::kModeRef, dimg, dtiles + g.offset, g.count, c->stream);
         if (e != cudaSuccess) return cuda_fail(e, "render kernel launch");
         g_launches.fetch_add(1, std::memory_order_relaxed);
     }

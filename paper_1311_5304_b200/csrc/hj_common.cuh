@@ -128,6 +128,25 @@ __device__ __forceinline__ Rgb colour(int y, int cb, int cr, bool &special, cons
     return Rgb{y + (rs >> kColK), y + (gs >> kColK), y + (bs >> kColK)};
 }
 
+// Colour of the islow (libjpeg) decode mode: jdcolor.c ycc_rgb_convert with
+// build_ycc_rgb_table (SCALEBITS 16, FIX(x) = (int)(x * 65536 + 0.5)):
+//   R = y + ((FIX(1.402) * (cr-128) + 2^15) >> 16), B likewise with FIX(1.772),
+//   G = y + ((-FIX(0.34414) * (cb-128) + 2^15 - FIX(0.71414) * (cr-128)) >> 16)
+// in the same IMAD + arithmetic-shift form (no float64 tie: exact integers).
+constexpr int kLjColK = 16;
+__device__ __forceinline__ ColourRegs colour_regs_libjpeg() {
+    ColourRegs k{32768 - 128 * 91881, 32768 - 128 * 116130, 32768 + 128 * (22554 + 46802), 91881, 116130,
+                 -22554, -46802};
+    asm("" : "+r"(k.cr), "+r"(k.cb), "+r"(k.cg), "+r"(k.ar), "+r"(k.ab), "+r"(k.agb), "+r"(k.agr));
+    return k;
+}
+__device__ __forceinline__ Rgb colour_libjpeg(int y, int cb, int cr, const ColourRegs &k) {
+    const int rs = k.ar * cr + k.cr;
+    const int bs = k.ab * cb + k.cb;
+    const int gs = k.agb * cb + (k.agr * cr + k.cg);
+    return Rgb{y + (rs >> kLjColK), y + (gs >> kLjColK), y + (bs >> kLjColK)};
+}
+
 // The tie-pair correction for one pixel (rarely executed).
 __device__ __forceinline__ int colour_g_exact(int y, int cb, int cr) {
     int g = y + ((HJ_COL_AGB * cb + HJ_COL_AGR * cr + HJ_COL_CG) >> kColK);

@@ -388,6 +388,81 @@ __device__ __forceinline__ bool screen_block(const int16_t *__restrict__ src, co
     else return screen_rows(src, qf, out);
 }
 
+// ------------------------------------------------- islow (libjpeg) mode
+// The "islow" decode mode (idct="islow"; north_star's libjpeg jidctint
+// fixed-point IDCT): libjpeg-turbo's jpeg_idct_islow (jidctint.c) in 32-bit
+// two's-complement arithmetic - CONST_BITS 13, PASS1_BITS 2, column pass
+// DESCALE(., 11) into an int workspace, row pass DESCALE(., 18), output
+// range_limit[x & 1023] = sat_u8(sext10(x) + 128) (jdmaster.c
+// prepare_range_limit_table).  Oracle: oracle/libjpeg_oracle.c, pinned to
+// libjpeg-turbo 3.1 (Pillow) decodes.  Exact integer arithmetic: no screen,
+// no float64 path.
+namespace lj {
+constexpr int F0298 = 2446, F0390 = 3196, F0541 = 4433, F0765 = 6270, F0899 = 7373, F1175 = 9633,
+              F1501 = 12299, F1847 = 15137, F1961 = 16069, F2053 = 16819, F2562 = 20995, F3072 = 25172;
+
+// one 1-D pass; o[k] = the pre-DESCALE output k (2^13-scaled).  Ring
+// arithmetic mod 2^32 (unsigned: wrapping is defined), signed only for the
+// arithmetic right shifts of DESCALE.
+typedef unsigned U;
+__device__ __forceinline__ void pass(const U (&i)[8], U (&o)[8]) {
+    const U z1e = (i[2] + i[6]) * (U)F0541;
+    const U t2e = z1e - i[6] * (U)F1847;
+    const U t3e = z1e + i[2] * (U)F0765;
+    const U t0e = (i[0] + i[4]) << 13;
+    const U t1e = (i[0] - i[4]) << 13;
+    const U t10 = t0e + t3e, t13 = t0e - t3e, t11 = t1e + t2e, t12 = t1e - t2e;
+    const U z1 = i[7] + i[1], z2 = i[5] + i[3], z3 = i[7] + i[3], z4 = i[5] + i[1];
+    const U z5 = (z3 + z4) * (U)F1175;
+    const U z3s = z5 - z3 * (U)F1961, z4s = z5 - z4 * (U)F0390;
+    const U t0 = i[7] * (U)F0298 - z1 * (U)F0899 + z3s;
+    const U t1 = i[5] * (U)F2053 - z2 * (U)F2562 + z4s;
+    const U t2 = i[3] * (U)F3072 - z2 * (U)F2562 + z3s;
+    const U t3 = i[1] * (U)F1501 - z1 * (U)F0899 + z4s;
+    o[0] = t10 + t3;
+    o[7] = t10 - t3;
+    o[1] = t11 + t2;
+    o[6] = t11 - t2;
+    o[2] = t12 + t1;
+    o[5] = t12 - t1;
+    o[3] = t13 + t0;
+    o[4] = t13 - t0;
+}
+// DESCALE(x, n) = (x + 2^(n-1)) >> n, arithmetic
+template <int N>
+__device__ __forceinline__ U descale(U x) { return (U)((int)(x + (1u << (N - 1))) >> N); }
+// range_limit[DESCALE(x, 18) & 1023] = sat_u8(sext10(.) + 128); pack4 saturates
+__device__ __forceinline__ int out_sample(U x) { return ((int)(descale<18>(x) << 22) >> 22) + 128; }
+}  // namespace lj
+
+__device__ __forceinline__ void islow_block(const int16_t *__restrict__ src, const int *qi, uint32_t (&out)[16]) {
+    int4 raw[8];
+    const int4 *s4 = reinterpret_cast<const int4 *>(src);
+#pragma unroll
+    for (int r = 0; r < 8; r += 2) ldg_rows2(s4 + r, raw[r], raw[r + 1]);
+    lj::U ws[8][8];  // ws[r][c]
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        lj::U in[8], o[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int w = c < 2 ? raw[r].x : c < 4 ? raw[r].y : c < 6 ? raw[r].z : raw[r].w;
+            const int coef = (c & 1) ? (w >> 16) : (int)(short)(w & 0xffff);
+            in[r] = (lj::U)coef * (lj::U)qi[r * 8 + c];  // DEQUANTIZE
+        }
+        lj::pass(in, o);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) ws[r][c] = lj::descale<11>(o[r]);  // CONST_BITS - PASS1_BITS
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        lj::U o[8];
+        lj::pass(ws[r], o);
+        out[2 * r] = pack4(lj::out_sample(o[0]), lj::out_sample(o[1]), lj::out_sample(o[2]), lj::out_sample(o[3]));
+        out[2 * r + 1] = pack4(lj::out_sample(o[4]), lj::out_sample(o[5]), lj::out_sample(o[6]), lj::out_sample(o[7]));
+    }
+}
+
 // ------------------------------------------------------ exact fallback
 
 // Cooperative exact float64 IDCT of one block by 8 threads (lane l = column
@@ -559,13 +634,24 @@ __device__ __forceinline__ int grab32(int *taken) {
 // Colour + pack of 4 pixels (Y bytes of `yw`, chroma ints) -> 12 RGB bytes
 // in 3 words.  Small live ranges on purpose: the colour constants stay in
 // registers instead of being rematerialised per pixel.
+template <int MODE>
+__device__ __forceinline__ Rgb colour_m(int y, int cb, int cr, bool &special, const ColourRegs &k) {
+    if constexpr (MODE == kModeIslow) return colour_libjpeg(y, cb, cr, k);
+    else return colour(y, cb, cr, special, k);
+}
+template <int MODE>
+__device__ __forceinline__ ColourRegs colour_regs_m() {
+    if constexpr (MODE == kModeIslow) return colour_regs_libjpeg();
+    else return colour_regs();
+}
+template <int MODE>
 __device__ __forceinline__ void colour4(uint32_t yw, int cb0, int cr0, int cb1, int cr1, int cb2, int cr2,
                                         int cb3, int cr3, bool &special, uint32_t &w0, uint32_t &w1,
                                         uint32_t &w2, const ColourRegs &k) {
-    const Rgb p0 = colour((int)__byte_perm(yw, 0, 0x4440), cb0, cr0, special, k);
-    const Rgb p1 = colour((int)__byte_perm(yw, 0, 0x4441), cb1, cr1, special, k);
-    const Rgb p2 = colour((int)__byte_perm(yw, 0, 0x4442), cb2, cr2, special, k);
-    const Rgb p3 = colour((int)__byte_perm(yw, 0, 0x4443), cb3, cr3, special, k);
+    const Rgb p0 = colour_m<MODE>((int)__byte_perm(yw, 0, 0x4440), cb0, cr0, special, k);
+    const Rgb p1 = colour_m<MODE>((int)__byte_perm(yw, 0, 0x4441), cb1, cr1, special, k);
+    const Rgb p2 = colour_m<MODE>((int)__byte_perm(yw, 0, 0x4442), cb2, cr2, special, k);
+    const Rgb p3 = colour_m<MODE>((int)__byte_perm(yw, 0, 0x4443), cb3, cr3, special, k);
     w0 = pack4(p0.r, p0.g, p0.b, p1.r);
     w1 = pack4(p1.g, p1.b, p2.r, p2.g);
     w2 = pack4(p2.b, p3.r, p3.g, p3.b);
@@ -687,22 +773,27 @@ __device__ __noinline__ void render16_exact(uint8_t *__restrict__ dst, uint4 yv,
 // under the 16 pixels), horizontal fancy filter even = 3c + prev + rnd_e,
 // odd = 3c + next + rnd_o with the result in byte 1 (Cb) / byte 3 (Cr) of
 // each lane; colour; 48 bytes stored at dst (cropped to npx).
+// MODE: kModeRef (the reference's float64 colour) or kModeIslow (libjpeg's
+// integer colour).  BOX: libjpeg's box replication instead of the triangle
+// filter (islow mode, chroma width <= 2): every neighbour reads as the
+// sample itself.
+template <int MODE, bool BOX = false>
 __device__ __forceinline__ void render16_swar(uint8_t *__restrict__ dst, uint4 yv, const uint32_t (&c)[10],
                                               uint32_t rnd_e, uint32_t rnd_o, int npx) {
     const uint32_t yw[4] = {yv.x, yv.y, yv.z, yv.w};
     uint32_t w[12];
     bool special = false;
-    const ColourRegs k = colour_regs();
+    const ColourRegs k = colour_regs_m<MODE>();
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const uint32_t ta = c[2 * q + 1] * 3u, tb = c[2 * q + 2] * 3u;
-        const uint32_t e0 = ta + c[2 * q] + rnd_e, o0 = ta + c[2 * q + 2] + rnd_o;
-        const uint32_t e1 = tb + c[2 * q + 1] + rnd_e, o1 = tb + c[2 * q + 3] + rnd_o;
-        colour4(yw[q], (int)__byte_perm(e0, 0, 0x4441), (int)(e0 >> 24), (int)__byte_perm(o0, 0, 0x4441),
+        const uint32_t e0 = ta + c[2 * q + (BOX ? 1 : 0)] + rnd_e, o0 = ta + c[2 * q + (BOX ? 1 : 2)] + rnd_o;
+        const uint32_t e1 = tb + c[2 * q + (BOX ? 2 : 1)] + rnd_e, o1 = tb + c[2 * q + (BOX ? 2 : 3)] + rnd_o;
+        colour4<MODE>(yw[q], (int)__byte_perm(e0, 0, 0x4441), (int)(e0 >> 24), (int)__byte_perm(o0, 0, 0x4441),
                 (int)(o0 >> 24), (int)__byte_perm(e1, 0, 0x4441), (int)(e1 >> 24),
                 (int)__byte_perm(o1, 0, 0x4441), (int)(o1 >> 24), special, w[3 * q], w[3 * q + 1], w[3 * q + 2], k);
     }
-    if (special) {
+    if (MODE == kModeRef && special) {
         render16_exact(dst, yv, make_uint4(c[0], c[1], c[2], c[3]), make_uint4(c[4], c[5], c[6], c[7]),
                        make_uint2(c[8], c[9]), rnd_e, rnd_o, 0, npx);
         return;
@@ -711,19 +802,20 @@ __device__ __forceinline__ void render16_swar(uint8_t *__restrict__ dst, uint4 y
 }
 
 // 16 pixels of a 4:4:4 row from Y / Cb / Cr byte vectors.
+template <int MODE>
 __device__ __forceinline__ void render16_444(uint8_t *__restrict__ dst, uint4 yv, uint4 bv, uint4 rv, int npx) {
     const uint32_t yw[4] = {yv.x, yv.y, yv.z, yv.w}, bw[4] = {bv.x, bv.y, bv.z, bv.w},
                    rw[4] = {rv.x, rv.y, rv.z, rv.w};
     uint32_t w[12];
     bool special = false;
-    const ColourRegs k = colour_regs();
+    const ColourRegs k = colour_regs_m<MODE>();
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-        colour4(yw[q], (int)(bw[q] & 0xff), (int)((rw[q]) & 0xff), (int)__byte_perm(bw[q], 0, 0x4441),
+        colour4<MODE>(yw[q], (int)(bw[q] & 0xff), (int)((rw[q]) & 0xff), (int)__byte_perm(bw[q], 0, 0x4441),
                 (int)__byte_perm(rw[q], 0, 0x4441), (int)__byte_perm(bw[q], 0, 0x4442),
                 (int)__byte_perm(rw[q], 0, 0x4442), (int)(bw[q] >> 24), (int)(rw[q] >> 24), special, w[3 * q],
                 w[3 * q + 1], w[3 * q + 2], k);
-    if (special) {
+    if (MODE == kModeRef && special) {
         render16_exact(dst, yv, bv, rv, make_uint2(0, 0), 0, 0, 1, npx);
         return;
     }
@@ -744,7 +836,18 @@ __device__ __forceinline__ void load_c10(const uint16_t *p, bool left_edge, bool
     c[9] = right_edge ? c[8] : widen(p[8]);
 }
 
-template <int SUB>
+// islow mode (libjpeg jdsample.c): the chroma plane's real width is
+// cw = ceil(w/2); the filter's right neighbour of column cw-1 is itself.
+// c[1 + j] holds chroma column c0 + j of the item (c[0], c[9] the
+// neighbours); columns from cw on only feed cropped pixels.
+__device__ __forceinline__ void lj_right_edge(uint32_t (&c)[10], int cw, int c0) {
+    const int j = cw - c0;  // window index of column cw
+#pragma unroll
+    for (int t = 1; t <= 8; ++t)
+        if (t == j) c[t + 1] = c[t];
+}
+
+template <int SUB, int MODE>
 __global__ void __launch_bounds__(kNT<SUB>, ctas_per_sm(SUB))
 render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ tiles) {
     using G = Geo<SUB>;
@@ -756,15 +859,21 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
     const int tid = threadIdx.x;
     const int mpr = im.mcus_per_row;
     const int S = t.m1 - t.m0;
-    const bool direct = (im.flags & HJ_FLAG_DIRECT_IDCT) != 0;
+    const bool direct = MODE == kModeRef && (im.flags & HJ_FLAG_DIRECT_IDCT) != 0;
+    constexpr bool kIslow = MODE == kModeIslow;
+    // islow: real chroma size (libjpeg downsampled_width / _height) and box
+    // replication instead of the triangle filter when it is <= 2 columns wide
+    const int lj_cw = (im.width + 1) >> 1, lj_ch = (im.height + 1) >> 1;
+    const bool lj_box = kIslow && lj_cw <= 2;
     constexpr int kThreads = kNT<SUB>;
     constexpr int kExactGroups = ::hj::kExactGroups<SUB>;
     for (int i = tid; i < 192; i += kThreads) {
         const int q = im.q[i];
         sm.qi[i >> 6][i & 63] = q;
     }
-    for (int i = tid; i < 192; i += kThreads)
-        sm.qf[i >> 6][qf_slot(kScreenCols<SUB>, (i & 63) >> 3, i & 7)] = (float)((double)im.q[i] * kPre64[i & 63]);
+    if constexpr (!kIslow)
+        for (int i = tid; i < 192; i += kThreads)
+            sm.qf[i >> 6][qf_slot(kScreenCols<SUB>, (i & 63) >> 3, i & 7)] = (float)((double)im.q[i] * kPre64[i & 63]);
     if (tid == 0) sm.n_queue[0] = sm.n_queue[1] = sm.n_taken[0] = sm.n_taken[1] = 0;
 
     const int cm_lo = (SUB == HJ_SUB_444) ? t.m0 : t.m0 - 1;  // first chroma window MCU
@@ -876,7 +985,12 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     uint32_t w[16];
                     const int comp = is_y ? 0 : 1 + k;
                     bool ok = false;
-                    if (!direct) ok = screen_block<SUB>(k ? srcB : srcA, sm.qf[comp], w);
+                    if constexpr (kIslow) {
+                        islow_block(k ? srcB : srcA, sm.qi[comp], w);
+                        ok = true;
+                    } else if (!direct) {
+                        ok = screen_block<SUB>(k ? srcB : srcA, sm.qf[comp], w);
+                    }
                     if (SUB == HJ_SUB_444 || is_y) {
                         // byte planes: Y (blocks side by side) or Cb / Cr
                         uint8_t *dst = is_y ? ydst + 8 * k : (k ? sm.crp[par] + 8 * lm : ydst);
@@ -987,10 +1101,19 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     const uint16_t *pn = cnear + p * G::CW + kw;
                     const uint16_t *pu = p > 0 ? pn - G::CW : (R > 0 ? cprev + kw : pn);
                     const uint16_t *pd = p < 7 ? pn + G::CW : (R + 1 < mcu_rows ? cnext + kw : pn);
+                    if (kIslow) {
+                        // libjpeg context rows: the real chroma plane ends at row
+                        // ceil(h/2) - 1 (jdmainct.c set_bottom_pointers); box
+                        // replication has no vertical filter
+                        if (lj_box || 8 * R + p >= lj_ch - 1) pd = pn;
+                        if (lj_box) pu = pn;
+                    }
                     const bool le = left_edge && g == 0, re = right_edge && g == S - 1;
+                    const int c0 = 8 * (t.m0 + g);  // the item's first chroma column
                     // colsum = 3*near + far per lane (libjpeg h2v2 fancy), 16x scaled
                     uint32_t n3[10];
                     load_c10(pn, le, re, n3);
+                    if (kIslow && c0 + 8 >= lj_cw) lj_right_edge(n3, lj_cw, c0);
 #pragma unroll
                     for (int k = 0; k < 10; ++k) n3[k] = n3[k] * (3u << G::CSH) + 0x00200020u;
                     const int rows = min(2, im.height - y0);
@@ -998,14 +1121,18 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     for (int h = 0; h < rows; ++h) {
                         uint32_t cs10[10];
                         load_c10(h ? pd : pu, le, re, cs10);
+                        if (kIslow && c0 + 8 >= lj_cw) lj_right_edge(cs10, lj_cw, c0);
 #pragma unroll
                         for (int k = 0; k < 10; ++k) cs10[k] = (cs10[k] << G::CSH) + n3[k];
                         // even 16(3cs+prev+8), odd 16(3cs+next+7): each colsum
                         // carries +2 (x16) from n3, so 3cs+prev already holds
                         // the +8 and odd subtracts 1 (lanes stay >= 0x80)
-                        render16_swar(im.rgb + ((int64_t)(y0 + h) * im.width + x0) * 3,
-                                      lds128(yp + (2 * p + h) * G::YW + 16 * g), cs10, 0u, 0u - 0x00100010u,
-                                      npx);
+                        uint8_t *dst = im.rgb + ((int64_t)(y0 + h) * im.width + x0) * 3;
+                        const uint4 yv = lds128(yp + (2 * p + h) * G::YW + 16 * g);
+                        if (kIslow && lj_box)
+                            render16_swar<MODE, true>(dst, yv, cs10, 0u, 0u - 0x00100010u, npx);
+                        else
+                            render16_swar<MODE>(dst, yv, cs10, 0u, 0u - 0x00100010u, npx);
                     }
                 }
             } else if constexpr (SUB == HJ_SUB_422) {
@@ -1026,12 +1153,18 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     if (npx <= 0) continue;
                     uint32_t c10[10];
                     load_c10(crow0 + y * G::CW + 8 * (g + 1), left_edge && g == 0, right_edge && g == S - 1, c10);
+                    const int c0 = 8 * (t.m0 + g);
+                    if (kIslow && c0 + 8 >= lj_cw) lj_right_edge(c10, lj_cw, c0);
 #pragma unroll
                     for (int k = 0; k < 10; ++k) c10[k] = (c10[k] << G::CSH) + 0x00100010u;
                     // h2v1 on 64x-scaled lanes: even 64(3c+prev+1), odd 64(3c+next+2);
                     // each sample carries +1/4 (x64), so 3c+prev already holds the +1
-                    render16_swar(im.rgb + ((int64_t)yy * im.width + x0) * 3, lds128(yp + y * G::YW + 16 * g),
-                                  c10, 0u, 0x00400040u, npx);
+                    uint8_t *dst = im.rgb + ((int64_t)yy * im.width + x0) * 3;
+                    const uint4 yv = lds128(yp + y * G::YW + 16 * g);
+                    if (kIslow && lj_box)
+                        render16_swar<MODE, true>(dst, yv, c10, 0u, 0x00400040u, npx);
+                    else
+                        render16_swar<MODE>(dst, yv, c10, 0u, 0x00400040u, npx);
                 }
             } else {
                 // item = (MCU pair g, row y): 16 pixels
@@ -1050,7 +1183,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     const int npx = min(min(16, im.width - x0), 8 * (S - 2 * g));
                     if (npx <= 0) continue;
                     const int o = y * G::YW + 16 * g;
-                    render16_444(im.rgb + ((int64_t)yy * im.width + x0) * 3, lds128(yp + o), lds128(cbp + o),
+                    render16_444<MODE>(im.rgb + ((int64_t)yy * im.width + x0) * 3, lds128(yp + o), lds128(cbp + o),
                                  lds128(crp + o), npx);
                 }
             }
@@ -1059,7 +1192,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
     }
 }
 
-template <int SUB>
+template <int SUB, int MODE>
 cudaError_t launch_sub(const hj_image_t *images, const Tile *tiles, int n_tiles, cudaStream_t stream) {
     // the dynamic shared-memory opt-in is per device; set it once per device
     // (thread-safe: a racing second setter is harmless and idempotent)
@@ -1070,11 +1203,11 @@ cudaError_t launch_sub(const hj_image_t *images, const Tile *tiles, int n_tiles,
     if (e != cudaSuccess) return e;
     const uint64_t bit = 1ull << (dev & 63);
     if (!(configured.load(std::memory_order_acquire) & bit)) {
-        e = cudaFuncSetAttribute(render_kernel<SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        e = cudaFuncSetAttribute(render_kernel<SUB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         if (e != cudaSuccess) return e;
         configured.fetch_or(bit, std::memory_order_release);
     }
-    render_kernel<SUB><<<n_tiles, kNT<SUB>, bytes, stream>>>(images, tiles);
+    render_kernel<SUB, MODE><<<n_tiles, kNT<SUB>, bytes, stream>>>(images, tiles);
     return cudaGetLastError();
 }
 
@@ -1091,12 +1224,19 @@ size_t render_smem_bytes(int sub) {
          : sub == HJ_SUB_422 ? sizeof(Smem<HJ_SUB_422>) : sizeof(Smem<HJ_SUB_420>);
 }
 
-cudaError_t launch_render(int sub, bool /*direct is per image*/, const hj_image_t *images, const Tile *tiles,
-                          int n_tiles, cudaStream_t stream) {
+// mode: kModeRef (AAN / direct chosen per image by HJ_FLAG_DIRECT_IDCT) or
+// kModeIslow (every image of the group decoded with libjpeg's arithmetic).
+cudaError_t launch_render(int sub, int mode, const hj_image_t *images, const Tile *tiles, int n_tiles,
+                          cudaStream_t stream) {
     if (n_tiles <= 0) return cudaSuccess;
-    if (sub == HJ_SUB_444) return launch_sub<HJ_SUB_444>(images, tiles, n_tiles, stream);
-    if (sub == HJ_SUB_422) return launch_sub<HJ_SUB_422>(images, tiles, n_tiles, stream);
-    return launch_sub<HJ_SUB_420>(images, tiles, n_tiles, stream);
+    if (mode == kModeIslow) {
+        if (sub == HJ_SUB_444) return launch_sub<HJ_SUB_444, kModeIslow>(images, tiles, n_tiles, stream);
+        if (sub == HJ_SUB_422) return launch_sub<HJ_SUB_422, kModeIslow>(images, tiles, n_tiles, stream);
+        return launch_sub<HJ_SUB_420, kModeIslow>(images, tiles, n_tiles, stream);
+    }
+    if (sub == HJ_SUB_444) return launch_sub<HJ_SUB_444, kModeRef>(images, tiles, n_tiles, stream);
+    if (sub == HJ_SUB_422) return launch_sub<HJ_SUB_422, kModeRef>(images, tiles, n_tiles, stream);
+    return launch_sub<HJ_SUB_420, kModeRef>(images, tiles, n_tiles, stream);
 }
 
 }  // namespace hj

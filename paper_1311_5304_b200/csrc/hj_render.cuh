@@ -66,9 +66,13 @@ inline int strip_width(int sub) {
     return sub == HJ_SUB_444 ? kStrip444 : sub == HJ_SUB_422 ? kStrip422 : kStrip420;
 }
 
+// Decode modes of the render kernel: the reference's float64 arithmetic
+// (AAN "fast" or "direct" per image flag) or libjpeg's integer "islow".
+enum { kModeRef = 0, kModeIslow = 1 };
+
 // Launch the render kernel for `n_tiles` tiles of one subsampling family.
 // `images` and `tiles` are device arrays.
-cudaError_t launch_render(int subsampling, bool direct, const hj_image_t *images,
+cudaError_t launch_render(int subsampling, int mode, const hj_image_t *images,
                           const Tile *tiles, int n_tiles, cudaStream_t stream);
 
 // Blocks the FP32 screen sent to the exact float64 path, all launches so far.

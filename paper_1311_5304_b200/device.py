@@ -101,10 +101,11 @@ class DeviceBatch:
     `geometries` lists ImageGeometry objects; each image gets a contiguous
     coefficient region [Y | Cb | Cr] (the host CoefficientBuffer layout, so
     one H2D copy moves it) and an RGB region (h*w*3).  `fast=False` selects
-    the direct-basis IDCT for every image.
+    the direct-basis IDCT for every image, `fast="islow"` libjpeg's integer
+    decode (the islow mode).
     """
 
-    def __init__(self, geometries, fast: bool = True):
+    def __init__(self, geometries, fast=True):
         _lib.require_device()
         self.slots = []
         coef = rgb = 0
@@ -139,7 +140,7 @@ class DeviceBatch:
         d.row0 = row0
         d.n_rows = g.mcu_rows - row0 if n_rows is None else n_rows
         d.subsampling = subsampling_code(g)
-        d.flags = 0 if self.fast else _lib.FLAG_DIRECT_IDCT
+        d.flags = _lib.image_flags(self.fast)
         return d
 
     def descs(self, items) -> C.Array:

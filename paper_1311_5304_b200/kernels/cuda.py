@@ -89,7 +89,7 @@ def _render(sub, y_blocks, cb_blocks, cr_blocks, qtables, rgb, width, height, mc
     st = _lib.lib.hj_render_rows(y_blocks.ctypes.data, cb_blocks.ctypes.data, cr_blocks.ctypes.data,
                                  q.ctypes.data, rgb.ctypes.data, int(width), int(height),
                                  int(mcus_per_row), mcu_rows, int(row0), int(n_rows), sub,
-                                 int(bool(fast)), int(bool(fused)), len(y_blocks), len(cb_blocks))
+                                 _lib.idct_code(fast), int(bool(fused)), len(y_blocks), len(cb_blocks))
     _lib.check(st, "render_rows")
 
 

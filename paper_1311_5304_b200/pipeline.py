@@ -23,7 +23,7 @@ class GpuLane:
     directions stay busy (the copy engines are independent: ~92 GB/s
     duplex on this box, tools/microbench/pcie.py)."""
 
-    def __init__(self, geometries, n_streams: int = 3, chunk: int = 4, fast: bool = True):
+    def __init__(self, geometries, n_streams: int = 3, chunk: int = 4, fast=True):
         self.batch = device.DeviceBatch(geometries, fast=fast)
         self.h2d, self.comp, self.d2h = device.Stream(), device.Stream(), device.Stream()
         self.streams = [self.h2d, self.comp, self.d2h]
@@ -91,7 +91,7 @@ class BatchDecoder:
     bound wall / huffman (orchestrator.py:71-75).
     """
 
-    def __init__(self, blobs, threads: int = 0, n_streams: int = 4, fast: bool = True):
+    def __init__(self, blobs, threads: int = 0, n_streams: int = 4, fast=True):
         import os
 
         from . import entropy, parser
