@@ -75,7 +75,28 @@ def parse_args():
                          "BASELINE config 4; 4:2:0 ranks also load one chroma MCU row of context)")
     ap.add_argument("--no-amdahl", action="store_true", help="skip the Huffman-inclusive pipeline run")
     ap.add_argument("--amdahl-images", type=int, default=32, help="images per rank in the pipeline run")
+    ap.add_argument("--idct", default="fast", choices=["fast", "direct", "islow"],
+                    help="fast/direct = the reference's float64 AAN / direct basis (bit-exact vs the reference); "
+                         "islow = libjpeg's integer decode (north_star's jidctint mode, exact vs libjpeg-turbo)")
     return ap.parse_args()
+
+
+def profile_key(args):
+    """Key of this workload's committed ncu capture in profiles/traffic.json."""
+    return args.workload + ("" if args.idct == "fast" else "_" + args.idct)
+
+
+def idct_arg(args):
+    """`fast` argument of the product API for --idct."""
+    return {"fast": True, "direct": False, "islow": "islow"}[args.idct]
+
+
+def oracle_render(c, q, w, h, sub, idct, threads):
+    """The CPU checker of one image for the chosen IDCT path (test oracle)."""
+    from oracle import oracle
+    if idct == "islow":
+        return oracle.render_islow(c.y_blocks, c.cb_blocks, c.cr_blocks, q, w, h, sub)
+    return oracle.render(c.y_blocks, c.cb_blocks, c.cr_blocks, q, w, h, sub, idct == "fast", threads)
 
 
 def dist_setup():
@@ -209,7 +230,7 @@ def ncu_traffic(workload):
         return None
 
 
-def cpu_baseline(images, wl, budget_s=3.0, variants=False):
+def cpu_baseline(images, wl, budget_s=3.0, variants=False, idct="fast"):
     """The reference's CPU path on this host's cores, bounded sample
     (>= budget_s of CPU work).  4:4:4 / 4:2:2: the reference itself
     (oracle/_ref, built from /root/reference) in one process per core;
@@ -221,6 +242,21 @@ def cpu_baseline(images, wl, budget_s=3.0, variants=False):
     sub = {"444": 0, "422": 1, "420": 2}[wl[3]]
     w, h = wl[0], wl[1]
     blobs = [b for b, _, _, _ in images[:2]]
+    if idct == "islow":
+        # libjpeg's integer parallel phase restated in C (oracle/libjpeg_oracle.c),
+        # one image per host thread (ctypes releases the GIL)
+        from concurrent.futures import ThreadPoolExecutor
+        t0 = time.perf_counter()
+        n = 0
+        with ThreadPoolExecutor(threads) as ex:
+            while time.perf_counter() - t0 < budget_s or n < threads:
+                list(ex.map(lambda k: oracle_render(images[k % len(images)][2], images[k % len(images)][3],
+                                                    w, h, sub, "islow", 1), range(n, n + threads)))
+                n += threads
+        dt = time.perf_counter() - t0
+        return {"value": round(n * w * h / dt / 1e6, 2), "unit": "Mpix/s", "cores": threads, "kind": "port",
+                "cpu": cpu_model(), "sample": f"{n} x {w}x{h} {wl[3]} images, {threads} threads, {dt:.1f} s wall "
+                "(oracle/libjpeg_oracle.c: libjpeg-turbo's jidctint/jdsample/jdcolor restated in C)"}
     if wl[3] != "420" and os.path.isdir(os.path.join(REF_DIR, "patched", "hetjpeg")):
         rate, n_img, wall, _ = reference_render_rate(blobs, wl[3], "patched", threads, budget_s)
         out = {"value": round(rate, 2), "unit": "Mpix/s", "cores": threads, "kind": "reference",
@@ -252,7 +288,7 @@ def cpu_baseline(images, wl, budget_s=3.0, variants=False):
                       "rejects 4:2:0, parser.py:223-229)"}
 
 
-def amdahl_run(images, wl, world, pg, n_images, reserve=0):
+def amdahl_run(images, wl, world, pg, n_images, reserve=0, idct="fast"):
     """Full decode of a batch (host Huffman on this rank's share of the host
     cores, pipelined with H2D -> kernel -> D2H on the B200) against the
     Huffman stage alone with the same decoder and threads:
@@ -261,18 +297,17 @@ def amdahl_run(images, wl, world, pg, n_images, reserve=0):
     from paper_1311_5304_b200.pipeline import BatchDecoder
     threads = max(1, len(os.sched_getaffinity(0)) // world - reserve)
     blobs = [images[i % len(images)][0] for i in range(n_images)]
-    dec = BatchDecoder(blobs, threads=threads, n_streams=4)
+    dec = BatchDecoder(blobs, threads=threads, n_streams=4, fast={"fast": True, "direct": False,
+                                                                  "islow": "islow"}[idct])
     try:
         dec.run()  # warm-up: plans, page-locked buffers
         huff, walls = [], []
         for _ in range(7):  # interleaved, so both see the same host conditions
             huff.append(dec.huffman_only())
             walls.append(dec.run()["wall_s"])
-        from oracle import oracle
         _, _, c0, q0 = images[0]
         w, h = wl[0], wl[1]
-        want = oracle.render(c0.y_blocks, c0.cb_blocks, c0.cr_blocks, q0, w, h,
-                             {"444": 0, "422": 1, "420": 2}[wl[3]], True, threads)
+        want = oracle_render(c0, q0, w, h, {"444": 0, "422": 1, "420": 2}[wl[3]], idct, threads)
         exact = bool(np.array_equal(dec.pixels[0].data, want))
     finally:
         dec.close()
@@ -589,7 +624,7 @@ def main():
     rows_mode = args.shard == "rows"
     images = make_inputs(wl, 0 if rows_mode else rank, batch)
     geos = [images[i % len(images)][2].geometry for i in range(batch)]
-    db = device.DeviceBatch(geos)
+    db = device.DeviceBatch(geos, fast=idct_arg(args))
     stream = device.Stream()
     g0 = geos[0]
     if rows_mode:
@@ -652,7 +687,7 @@ def main():
     achieved = bytes_step / (kernel_ms / 1e3) / 1e9
 
     # ---- end to end through the public host API (pinned H2D -> kernel -> D2H)
-    lane = pipeline.GpuLane(geos, chunk=args.e2e_chunk)
+    lane = pipeline.GpuLane(geos, chunk=args.e2e_chunk, fast=idct_arg(args))
     from paper_1311_5304_b200.entropy import PinnedArray
     outs = [PinnedArray((g.height, g.width, 3), np.uint8) for g in geos]
     out_arrays = [o.array for o in outs]
@@ -704,7 +739,7 @@ def main():
 
     def one(i):
         c = coeffs[i]
-        fn(c.y_blocks, c.cb_blocks, c.cr_blocks, qts[i], out_arrays[i], w, h, mpr, row0, n_rows)
+        fn(c.y_blocks, c.cb_blocks, c.cr_blocks, qts[i], out_arrays[i], w, h, mpr, row0, n_rows, idct_arg(args))
 
     n_thr = args.e2e_threads
     with ThreadPoolExecutor(n_thr) as ex:
@@ -718,29 +753,27 @@ def main():
     e2e_value = px_all * e2e_steps / e2e_s / 1e6
     e2e_lane_value = px_all * e2e_steps / e2e_lane_s / 1e6
     # the e2e output must be the kernel's output: spot-check one image against the oracle
-    from oracle import oracle
     _, _, c0, q0 = images[0]
-    want = oracle.render(c0.y_blocks, c0.cb_blocks, c0.cr_blocks, q0, w, h,
-                         {"444": 0, "422": 1, "420": 2}[sub], True,
+    want = oracle_render(c0, q0, w, h, {"444": 0, "422": 1, "420": 2}[sub], args.idct,
                          len(os.sched_getaffinity(0)))
     exact = bool(np.array_equal(out_arrays[0][y_lo:y_hi], want[y_lo:y_hi]))
 
     # ---- end to end INCLUDING host Huffman: the paper's Amdahl metric
     amdahl = None
     if not args.no_amdahl:
-        amdahl = amdahl_run(images, wl, world, pg, args.amdahl_images)
+        amdahl = amdahl_run(images, wl, world, pg, args.amdahl_images, idct=args.idct)
         # the same with one host core left to the GPU submission thread and
         # the driver (both legs on the remaining cores): all-cores Huffman
         # is fastest, but its workers then get preempted by the pipeline
         cores = len(os.sched_getaffinity(0)) // world
         if cores > 2:
-            r = amdahl_run(images, wl, world, pg, args.amdahl_images, reserve=1)
+            r = amdahl_run(images, wl, world, pg, args.amdahl_images, reserve=1, idct=args.idct)
             amdahl["one_core_reserved"] = {k: r[k] for k in ("t_huff_ms", "t_wall_ms", "frac_of_bound",
                                                              "mpix_s", "host_threads_per_rank")}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(images, wl, variants=args.cpu_variants)
+        cpu = cpu_baseline(images, wl, variants=args.cpu_variants, idct=args.idct)
 
     if rank == 0:
         line = {
@@ -748,9 +781,10 @@ def main():
             "value": round(value, 1), "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5),
             "higher_is_better": True, "scaling": "strong" if rows_mode else "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{w}x{h} {sub} q{q}" + (" rst" if rst else ""),
-                       "images_per_step_per_gpu": batch, "distinct_images": len(images),
+            "dtype": "int32" if args.idct == "islow" else "f64", "data": "synthetic",
+            "config": {"workload": f"{w}x{h} {sub} q{q}" + (" rst" if rst else "")
+                       + ("" if args.idct == "fast" else f" idct={args.idct}"),
+                       "idct": args.idct, "images_per_step_per_gpu": batch, "distinct_images": len(images),
                        "bytes_per_step_per_gpu": bytes_step,
                        "l2": "inputs > L2 (coefficients %.0f MB/step/GPU)" % (
                            sum(s.coef_bytes for s in db.slots) / 1e6),
@@ -759,7 +793,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
-                         "traffic": ncu_traffic(args.workload) if args.batch == 0 else None,
+                         "traffic": ncu_traffic(profile_key(args)) if args.batch == 0 else None,
                          "kernel_ms": round(kernel_ms, 5)},
             "e2e": {"value": round(e2e_value, 1), "unit": "Mpix/s",
                     "h2d_bytes_per_step": io["h2d_bytes"], "d2h_bytes_per_step": io["d2h_bytes"],
@@ -770,7 +804,7 @@ def main():
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "amdahl": amdahl,
-            "issue_roofline": issue_roofline(args.workload, value, clk.get("sm_mhz"), world)
+            "issue_roofline": issue_roofline(profile_key(args), value, clk.get("sm_mhz"), world)
             if args.batch == 0 and not rows_mode else None,
             "idct_screen": {"exact_fp64_block_frac": round(
                 exact_blocks / (args.steps * (batch * n_rows * g0.mcus_per_row * (g0.y_blocks_per_mcu + 2)
