@@ -235,6 +235,39 @@ hj_status hj_pipeline_run(const hj_pipe_image_t *images, int32_t n_images, int32
 /* The same host stage alone (T_huff of the Amdahl bound, orchestrator.py:71-75). */
 hj_status hj_pipeline_huffman(const hj_pipe_image_t *images, int32_t n_images, int32_t n_threads);
 
+/* ---- streaming decode with a bounded ring (BASELINE config 5) ---------
+ * One image of a stream: its scan (hj_huff_build tables + entropy-coded
+ * bytes), its host qtables and its geometry.  rgb_out: host destination of
+ * its RGB (page-locked for an asynchronous copy), or NULL to leave it in the
+ * ring's own page-locked slot (delivered and then overwritten). */
+typedef struct {
+    const void *huff;
+    const uint8_t *scan;
+    int64_t scan_bytes;
+    const int32_t *q;                     /* (3, 64) host qtables */
+    int32_t width, height, subsampling;   /* HJ_SUB_* */
+    int32_t flags;                        /* HJ_FLAG_* (IDCT path) */
+    int32_t restart_interval;
+    uint8_t *rgb_out;
+} hj_stream_image_t;
+
+typedef struct {
+    int64_t images, launches;
+    int64_t h2d_bytes, d2h_bytes;         /* moved by the GPU leg */
+    int64_t pinned_bytes, device_bytes;   /* the ring's whole footprint */
+    double huffman_thread_s;              /* summed host entropy-decode time */
+} hj_stream_stats_t;
+
+/* Decode n images in list order with n_slots reusable slots (page-locked
+ * planes + device planes + stream each, sized to the largest image): n_threads
+ * host threads Huffman-decode into free slots; the calling thread queues each
+ * decoded slot's H2D -> render -> D2H and recycles finished slots.  Memory is
+ * bounded by the slots, not the list.  gpu = 0: the host stage alone (T_huff).
+ * Replaces the reference's per-image decode loop (cli.py:175-234) for a
+ * whole corpus; first error wins. */
+hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, int32_t n_threads, int32_t n_slots,
+                        int32_t gpu, hj_stream_stats_t *stats);
+
 /* Index of the first non-restart marker after the scan data starting at
  * `start`, or -1 if the stream ends inside the entropy-coded data
  * (parser.py:277-293, _scan_entropy_end). */

@@ -91,6 +91,21 @@ class hj_pipe_image_t(C.Structure):  # noqa: N801
     ]
 
 
+class hj_stream_image_t(C.Structure):  # noqa: N801
+    _fields_ = [
+        ("huff", C.c_void_p), ("scan", C.c_void_p), ("scan_bytes", C.c_int64), ("q", C.c_void_p),
+        ("width", C.c_int32), ("height", C.c_int32), ("subsampling", C.c_int32), ("flags", C.c_int32),
+        ("restart_interval", C.c_int32), ("rgb_out", C.c_void_p),
+    ]
+
+
+class hj_stream_stats_t(C.Structure):  # noqa: N801
+    _fields_ = [
+        ("images", C.c_int64), ("launches", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+        ("pinned_bytes", C.c_int64), ("device_bytes", C.c_int64), ("huffman_thread_s", C.c_double),
+    ]
+
+
 if not os.path.exists(_LIB_PATH):
     raise ImportError(
         f"native library missing: {_LIB_PATH} (build it with "
@@ -143,6 +158,8 @@ _SIG = {
     "hj_huff_free": (None, [_P]),
     "hj_decode_scan_fast": (C.c_int, [_P, _P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _I32]),
     "hj_pipeline_run": (C.c_int, [C.POINTER(hj_pipe_image_t), _I32, _I32, C.POINTER(_P)]),
+    "hj_stream_run": (C.c_int, [C.POINTER(hj_stream_image_t), _I32, _I32, _I32, _I32,
+                                C.POINTER(hj_stream_stats_t)]),
     "hj_pipeline_huffman": (C.c_int, [C.POINTER(hj_pipe_image_t), _I32, _I32]),
 }
 for _name, (_res, _args) in _SIG.items():

@@ -5,6 +5,7 @@
 // launches, and thin wrappers over device memory so a host language needs
 // nothing but this library (ctypes, cgo, JNI ...).
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <condition_variable>
 #include <cstdlib>
@@ -793,3 +794,284 @@ hj_status hj_upsample_422(const uint8_t *rows, const int16_t *left, const int16_
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Streaming decode with a bounded ring of slots (BASELINE config 5: 10k
+// mixed images; memory stays O(slots x largest image), not O(batch)).
+//
+// Host worker threads take the next image, wait for a free slot and
+// Huffman-decode into its page-locked coefficient planes; the calling thread
+// alone talks to the CUDA driver (the pipeline's lesson: workers inside the
+// driver slow each other down): for each decoded slot it uploads the
+// coefficients and the image's tile plan, launches the render kernel and
+// queues the RGB D2H - all on the slot's own stream - and recycles slots
+// whose completion event has fired.  gpu = 0 runs the host stage alone
+// (T_huff of the Amdahl bound, orchestrator.py:71-75).
+namespace {
+
+struct StreamSlot {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+    int16_t *h_coef = nullptr;  // pinned planes [Y | Cb | Cr]
+    uint8_t *h_rgb = nullptr;   // pinned ring RGB (images without rgb_out)
+    uint8_t *h_plan = nullptr;  // pinned [q 1 KB][image desc 256 B][tiles]
+    void *d_coef = nullptr, *d_rgb = nullptr, *d_misc = nullptr;
+    int image = -1;
+    int status = HJ_OK;
+};
+
+size_t stream_coef_bytes(const hj_stream_image_t &im) {
+    const int mw = mcu_w_of(im.subsampling), mh = mcu_h_of(im.subsampling);
+    const int64_t mcus = (int64_t)((im.width + mw - 1) / mw) * ((im.height + mh - 1) / mh);
+    return (size_t)mcus * (ypm_of(im.subsampling) + 2) * 128;
+}
+
+}  // namespace
+
+extern "C" hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, int32_t n_threads,
+                                   int32_t n_slots, int32_t gpu, hj_stream_stats_t *stats) {
+    if (n < 0 || (n > 0 && !images) || n_threads < 1 || n_slots < 1)
+        return fail(HJ_ERR_ARG, "stream: bad image array, thread or slot count");
+    hj_stream_stats_t local{};
+    hj_stream_stats_t &st = stats ? *stats : local;
+    st = hj_stream_stats_t{};
+    if (n == 0) return HJ_OK;
+    size_t max_coef = 0, max_rgb = 0;
+    for (int i = 0; i < n; ++i) {
+        const hj_stream_image_t &im = images[i];
+        if (!im.huff || (!im.scan && im.scan_bytes) || !im.q || im.subsampling < HJ_SUB_444 ||
+            im.subsampling > HJ_SUB_420 || im.width < 1 || im.height < 1)
+            return fail(HJ_ERR_ARG, "stream: image " + std::to_string(i) + ": bad descriptor");
+        max_coef = std::max(max_coef, stream_coef_bytes(im));
+        max_rgb = std::max(max_rgb, (size_t)im.width * im.height * 3);
+    }
+    const size_t plan_bytes = 1024 + 256 + sizeof(hj::Tile) * 65536;
+    std::vector<StreamSlot> slots((size_t)n_slots);
+    auto release = [&]() {
+        for (auto &sl : slots) {
+            if (sl.stream) cudaStreamSynchronize(sl.stream);
+            if (gpu) cudaFreeHost(sl.h_coef);
+            else std::free(sl.h_coef);
+            cudaFreeHost(sl.h_rgb);
+            cudaFreeHost(sl.h_plan);
+            cudaFree(sl.d_coef);
+            cudaFree(sl.d_rgb);
+            cudaFree(sl.d_misc);
+            if (sl.done) cudaEventDestroy(sl.done);
+            if (sl.stream) cudaStreamDestroy(sl.stream);
+        }
+    };
+    // allocation (outside any timing the caller does around the decode proper
+    // is the caller's business; counted in stats)
+    for (auto &sl : slots) {
+        // the host-only run (gpu = 0) needs no driver: plain memory
+        cudaError_t e = cudaSuccess;
+        if (gpu) e = cudaHostAlloc(reinterpret_cast<void **>(&sl.h_coef), max_coef, cudaHostAllocDefault);
+        else if (!(sl.h_coef = static_cast<int16_t *>(std::malloc(max_coef)))) e = cudaErrorMemoryAllocation;
+        if (e == cudaSuccess && gpu) e = cudaHostAlloc(reinterpret_cast<void **>(&sl.h_rgb), max_rgb, cudaHostAllocDefault);
+        if (e == cudaSuccess && gpu) e = cudaHostAlloc(reinterpret_cast<void **>(&sl.h_plan), plan_bytes, cudaHostAllocDefault);
+        if (e == cudaSuccess && gpu) e = cudaMalloc(&sl.d_coef, max_coef);
+        if (e == cudaSuccess && gpu) e = cudaMalloc(&sl.d_rgb, max_rgb);
+        if (e == cudaSuccess && gpu) e = cudaMalloc(&sl.d_misc, plan_bytes);
+        if (e == cudaSuccess && gpu) e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess && gpu) e = cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            release();
+            return cuda_fail(e, "stream: slot allocation");
+        }
+    }
+    st.pinned_bytes = (int64_t)n_slots * (int64_t)(max_coef + (gpu ? max_rgb + plan_bytes : 0));
+    st.device_bytes = gpu ? (int64_t)n_slots * (int64_t)(max_coef + max_rgb + plan_bytes) : 0;
+
+    std::mutex mu;
+    std::condition_variable cv_free, cv_ready;
+    std::vector<int> free_slots, ready;  // slot indices
+    for (int k = n_slots - 1; k >= 0; --k) free_slots.push_back(k);
+    std::atomic<int> next{0};
+    std::atomic<int> first_err{HJ_OK};
+    std::string err_msg;
+    std::atomic<int64_t> huff_ns{0};
+    int decoded = 0;  // images whose host stage ended (ok or not), under mu
+
+    auto worker = [&]() {
+        for (;;) {
+            const int i = next.fetch_add(1);
+            if (i >= n || first_err.load() != HJ_OK) {
+                if (i < n) {
+                    std::lock_guard<std::mutex> g(mu);
+                    ++decoded;  // skipped after an error
+                    cv_ready.notify_one();
+                }
+                if (i >= n) return;
+                continue;
+            }
+            int k;
+            {
+                std::unique_lock<std::mutex> g(mu);
+                cv_free.wait(g, [&] { return !free_slots.empty(); });
+                k = free_slots.back();
+                free_slots.pop_back();
+            }
+            StreamSlot &sl = slots[k];
+            const hj_stream_image_t &im = images[i];
+            const size_t cb = stream_coef_bytes(im);
+            const int mw = mcu_w_of(im.subsampling), mh = mcu_h_of(im.subsampling);
+            const int mpr = (im.width + mw - 1) / mw, rows = (im.height + mh - 1) / mh;
+            const int64_t nc = (int64_t)mpr * rows, ny = nc * ypm_of(im.subsampling);
+            const auto t0 = std::chrono::steady_clock::now();
+            int s = hj_decode_scan_fast(im.huff, im.scan, im.scan_bytes, sl.h_coef, sl.h_coef + ny * 64,
+                                        sl.h_coef + (ny + nc) * 64, mpr, rows, ypm_of(im.subsampling),
+                                        im.restart_interval, 1);
+            huff_ns.fetch_add(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                  std::chrono::steady_clock::now() - t0).count());
+            (void)cb;
+            std::lock_guard<std::mutex> g(mu);
+            if (s != HJ_OK) {
+                int expect = HJ_OK;
+                if (first_err.compare_exchange_strong(expect, s))
+                    err_msg = "image " + std::to_string(i) + ": " + t_error;
+                free_slots.push_back(k);
+                cv_free.notify_one();
+            } else {
+                sl.image = i;
+                ready.push_back(k);
+            }
+            ++decoded;
+            cv_ready.notify_one();
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < n_threads; ++t) pool.emplace_back(worker);
+
+    // submitter (this thread): the only CUDA caller
+    hj_status sub_err = HJ_OK;
+    std::vector<int> inflight;
+    std::vector<int> batch;
+    auto recycle = [&](bool block) {
+        for (size_t j = 0; j < inflight.size();) {
+            StreamSlot &sl = slots[inflight[j]];
+            cudaError_t e = block && j == 0 ? cudaEventSynchronize(sl.done) : cudaEventQuery(sl.done);
+            if (e == cudaErrorNotReady) {
+                (void)cudaGetLastError();  // a pending event is not an error to report later
+                ++j;
+                continue;
+            }
+            if (e != cudaSuccess && sub_err == HJ_OK) sub_err = cuda_fail(e, "stream: image completion");
+            {
+                std::lock_guard<std::mutex> g(mu);
+                free_slots.push_back(inflight[j]);
+            }
+            cv_free.notify_one();
+            inflight.erase(inflight.begin() + (long)j);
+            block = false;
+        }
+    };
+    for (;;) {
+        int done_now;
+        {
+            std::unique_lock<std::mutex> g(mu);
+            if (ready.empty() && decoded < n) {
+                if (inflight.empty()) cv_ready.wait(g, [&] { return !ready.empty() || decoded == n; });
+                else cv_ready.wait_for(g, std::chrono::microseconds(50), [&] { return !ready.empty() || decoded == n; });
+            }
+            batch.swap(ready);
+            done_now = decoded;
+        }
+        for (int k : batch) {
+            StreamSlot &sl = slots[k];
+            const hj_stream_image_t &src = images[sl.image];
+            if (!gpu || sub_err != HJ_OK || first_err.load() != HJ_OK) {
+                std::lock_guard<std::mutex> g(mu);
+                free_slots.push_back(k);
+                cv_free.notify_one();
+                continue;
+            }
+            hj_image_t im{};
+            im.width = src.width;
+            im.height = src.height;
+            const int mw = mcu_w_of(src.subsampling), mh = mcu_h_of(src.subsampling);
+            im.mcus_per_row = (src.width + mw - 1) / mw;
+            im.mcu_rows = (src.height + mh - 1) / mh;
+            im.row0 = 0;
+            im.n_rows = im.mcu_rows;
+            im.subsampling = src.subsampling;
+            im.flags = src.flags;
+            const int64_t nc = (int64_t)im.mcus_per_row * im.mcu_rows, ny = nc * ypm_of(src.subsampling);
+            int16_t *dy = static_cast<int16_t *>(sl.d_coef);
+            im.y = dy;
+            im.cb = dy + ny * 64;
+            im.cr = dy + (ny + nc) * 64;
+            uint8_t *misc = static_cast<uint8_t *>(sl.d_misc);
+            im.q = reinterpret_cast<const int32_t *>(misc);
+            im.rgb = static_cast<uint8_t *>(sl.d_rgb);
+            hj_status vs = validate(im);
+            std::vector<hj::Tile> tiles;
+            std::vector<Plan::Group> groups;
+            if (vs == HJ_OK) {
+                build_tiles(&im, 1, tiles, groups);
+                if (1024 + 256 + sizeof(hj::Tile) * tiles.size() > plan_bytes) vs = fail(HJ_ERR_ARG, "stream: tile plan too large");
+            }
+            if (vs != HJ_OK) {
+                sub_err = vs;
+                std::lock_guard<std::mutex> g(mu);
+                free_slots.push_back(k);
+                cv_free.notify_one();
+                continue;
+            }
+            std::memcpy(sl.h_plan, src.q, 768);
+            std::memcpy(sl.h_plan + 1024, &im, sizeof(im));
+            std::memcpy(sl.h_plan + 1024 + 256, tiles.data(), sizeof(hj::Tile) * tiles.size());
+            const size_t coef_b = (size_t)(ny + 2 * nc) * 128, rgb_b = (size_t)src.width * src.height * 3;
+            const size_t plan_b = 1024 + 256 + sizeof(hj::Tile) * tiles.size();
+            cudaError_t e = cudaMemcpyAsync(sl.d_coef, sl.h_coef, coef_b, cudaMemcpyHostToDevice, sl.stream);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(misc, sl.h_plan, plan_b, cudaMemcpyHostToDevice, sl.stream);
+            for (const auto &gr : groups) {
+                if (e != cudaSuccess) break;
+                e = hj::launch_render(gr.sub, gr.kind == 2 ? hj::kModeIslow : hj::kModeRef,
+                                      reinterpret_cast<const hj_image_t *>(misc + 1024),
+                                      reinterpret_cast<const hj::Tile *>(misc + 1024 + 256) + gr.offset, gr.count,
+                                      sl.stream);
+                if (e == cudaSuccess) {
+                    g_launches.fetch_add(1, std::memory_order_relaxed);
+                    ++st.launches;
+                }
+            }
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(src.rgb_out ? src.rgb_out : sl.h_rgb, sl.d_rgb, rgb_b, cudaMemcpyDeviceToHost,
+                                    sl.stream);
+            if (e == cudaSuccess) e = cudaEventRecord(sl.done, sl.stream);
+            if (e != cudaSuccess) {
+                if (sub_err == HJ_OK) sub_err = cuda_fail(e, "stream: queue image");
+                cudaStreamSynchronize(sl.stream);
+                std::lock_guard<std::mutex> g(mu);
+                free_slots.push_back(k);
+                cv_free.notify_one();
+                continue;
+            }
+            st.h2d_bytes += (int64_t)(coef_b + plan_b);
+            st.d2h_bytes += (int64_t)rgb_b;
+            ++st.images;
+            inflight.push_back(k);
+        }
+        batch.clear();
+        // a worker blocked on a full ring needs a slot back: block on the
+        // oldest in-flight image when no slot is free
+        bool starving;
+        {
+            std::lock_guard<std::mutex> g(mu);
+            starving = free_slots.empty();
+        }
+        recycle(starving && !inflight.empty());
+        if (done_now == n) {
+            std::lock_guard<std::mutex> g(mu);
+            if (ready.empty()) break;
+        }
+    }
+    while (!inflight.empty()) recycle(true);
+    for (auto &th : pool) th.join();
+    st.huffman_thread_s = (double)huff_ns.load() * 1e-9;
+    if (!gpu) st.images = n;
+    release();
+    if (first_err.load() != HJ_OK) return fail((hj_status)first_err.load(), "stream: " + err_msg);
+    return sub_err;
+}

@@ -208,3 +208,90 @@ class BatchDecoder:
 
     def close(self):
         self.batch.close()
+
+
+class StreamDecoder:
+    """Whole-corpus decode with bounded memory (BASELINE config 5: 10k mixed
+    images): a ring of `slots` reusable page-locked + device slots sized to
+    the largest image (hj_stream_run).  Host threads Huffman-decode into free
+    slots; the calling thread queues each slot's H2D -> render -> D2H and
+    recycles finished ones - memory is O(slots), not O(corpus), unlike
+    BatchDecoder, which keeps every image resident.
+
+    `blobs` may repeat the same bytes object (a corpus drawn from a pool):
+    each distinct blob is parsed and gets its Huffman tables once.  `keep`:
+    indices whose RGB is copied out to page-locked arrays (self.kept[i]);
+    the others are delivered into the ring and overwritten.  `order`: the
+    processing order (default: largest first, which shortens the tail)."""
+
+    def __init__(self, blobs, threads: int = 0, slots: int = 0, fast=True, keep=(), order=None):
+        import ctypes as C
+        import os
+
+        from . import entropy, parser
+        from .perf_model import qtable_stack
+        self.threads = threads or len(os.sched_getaffinity(0))
+        self.slots = slots or self.threads + 4
+        self._distinct = {}
+        self._keep_alive = []
+        per = []
+        for b in blobs:
+            key = id(b)
+            if key not in self._distinct:
+                p = parser.parse_stream(b)
+                fs = entropy.FastScan(p)
+                sp = p.entropy_span
+                view = np.frombuffer(b, dtype=np.uint8)[sp.offset:sp.offset + sp.length]
+                q = np.ascontiguousarray(qtable_stack(p), np.int32)
+                self._distinct[key] = (b, p, fs, view, q)
+            per.append(self._distinct[key])
+        self.n = len(per)
+        self.geometries = [d[2].geometry for d in per]
+        self.pixels = sum(g.width * g.height for g in self.geometries)
+        if order is None:
+            order = sorted(range(self.n), key=lambda i: -self.geometries[i].width * self.geometries[i].height)
+        self.order = list(order)
+        self.kept = {}
+        keep = set(keep) if _lib.lib.hj_device_count() > 0 else set()  # page-locked outputs need a driver
+        arr = (_lib.hj_stream_image_t * max(1, self.n))()
+        for k, i in enumerate(self.order):
+            b, p, fs, view, q = per[i]
+            g = self.geometries[i]
+            d = arr[k]
+            d.huff = fs._h
+            d.scan, d.scan_bytes = view.ctypes.data, len(view)
+            d.q = q.ctypes.data
+            d.width, d.height = g.width, g.height
+            d.subsampling = device.subsampling_code(g)
+            d.flags = _lib.image_flags(fast)
+            d.restart_interval = p.restart_interval
+            if i in keep:
+                out = PinnedArray((g.height, g.width, 3), np.uint8)
+                self.kept[i] = out
+                d.rgb_out = out.array.ctypes.data
+        self._arr = arr
+        self._C = C
+
+    def _run(self, gpu: int) -> dict:
+        import time
+        stats = _lib.hj_stream_stats_t()
+        t0 = time.perf_counter()
+        _lib.check(_lib.lib.hj_stream_run(self._arr, self.n, self.threads, self.slots, gpu,
+                                          self._C.byref(stats)), "hj_stream_run")
+        wall = time.perf_counter() - t0
+        return {"wall_s": wall, "images": stats.images, "launches": stats.launches,
+                "h2d_bytes": stats.h2d_bytes, "d2h_bytes": stats.d2h_bytes,
+                "pinned_bytes": stats.pinned_bytes, "device_bytes": stats.device_bytes,
+                "huffman_thread_s": stats.huffman_thread_s}
+
+    def run(self) -> dict:
+        """Decode the whole corpus (host Huffman pipelined with the B200)."""
+        _lib.require_device()
+        return self._run(1)
+
+    def huffman_only(self) -> dict:
+        """The same host stage alone: same decoder, threads and ring (T_huff)."""
+        return self._run(0)
+
+    def rgb(self, i: int) -> np.ndarray:
+        return self.kept[i].array
