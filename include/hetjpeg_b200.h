@@ -208,6 +208,16 @@ hj_status hj_decode_scan_fast(const void *fast, const uint8_t *data, int64_t n_b
                               int32_t mcus_per_row, int32_t mcu_rows, int32_t y_per_mcu,
                               int32_t restart_interval, int32_t n_threads);
 
+/* MCU rows [row0, row0+n_rows) of a scan: only the restart intervals that
+ * cover them are Huffman-decoded (their blocks written, zeros included), on up
+ * to n_threads threads - a shard of one large image (BASELINE config 4,
+ * MCU-row shards across GPUs) pays only for its own intervals.  Without
+ * restart intervals the whole scan is decoded. */
+hj_status hj_decode_scan_rows(const void *fast, const uint8_t *data, int64_t n_bytes,
+                              int16_t *y_out, int16_t *cb_out, int16_t *cr_out,
+                              int32_t mcus_per_row, int32_t mcu_rows, int32_t y_per_mcu,
+                              int32_t restart_interval, int32_t row0, int32_t n_rows, int32_t n_threads);
+
 /* ---- native batch pipeline (pipeline.BatchDecoder; the paper's pipelined
  * host-Huffman / accelerator scheme, §5.3, at batch granularity).
  * One image: its scan (hj_huff_build tables + entropy-coded bytes), its
@@ -249,6 +259,10 @@ typedef struct {
     int32_t flags;                        /* HJ_FLAG_* (IDCT path) */
     int32_t restart_interval;
     uint8_t *rgb_out;
+    int32_t row0, n_rows;                 /* MCU rows to decode and render (n_rows 0 = all): an
+                                             image shard - only its restart intervals are
+                                             Huffman-decoded (4:2:0: plus one chroma MCU row of
+                                             context each side) and only its RGB rows move */
 } hj_stream_image_t;
 
 typedef struct {

@@ -95,7 +95,7 @@ class hj_stream_image_t(C.Structure):  # noqa: N801
     _fields_ = [
         ("huff", C.c_void_p), ("scan", C.c_void_p), ("scan_bytes", C.c_int64), ("q", C.c_void_p),
         ("width", C.c_int32), ("height", C.c_int32), ("subsampling", C.c_int32), ("flags", C.c_int32),
-        ("restart_interval", C.c_int32), ("rgb_out", C.c_void_p),
+        ("restart_interval", C.c_int32), ("rgb_out", C.c_void_p), ("row0", C.c_int32), ("n_rows", C.c_int32),
     ]
 
 
@@ -157,6 +157,7 @@ _SIG = {
     "hj_huff_build": (C.c_int, [C.POINTER(hj_scan_tables_t), C.POINTER(_P)]),
     "hj_huff_free": (None, [_P]),
     "hj_decode_scan_fast": (C.c_int, [_P, _P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _I32]),
+    "hj_decode_scan_rows": (C.c_int, [_P, _P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32]),
     "hj_pipeline_run": (C.c_int, [C.POINTER(hj_pipe_image_t), _I32, _I32, C.POINTER(_P)]),
     "hj_stream_run": (C.c_int, [C.POINTER(hj_stream_image_t), _I32, _I32, _I32, _I32,
                                 C.POINTER(hj_stream_stats_t)]),

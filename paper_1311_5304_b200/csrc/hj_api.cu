@@ -826,6 +826,22 @@ size_t stream_coef_bytes(const hj_stream_image_t &im) {
     return (size_t)mcus * (ypm_of(im.subsampling) + 2) * 128;
 }
 
+// Coefficient MCU rows a stream item needs: its own rows, and for 4:2:0 one
+// chroma MCU row of context on each side (the vertical filter).
+void stream_coef_rows(const hj_stream_image_t &im, int rows, int &lo, int &hi) {
+    if (im.n_rows <= 0) {
+        lo = 0;
+        hi = rows;
+        return;
+    }
+    lo = im.row0;
+    hi = im.row0 + im.n_rows;
+    if (im.subsampling == HJ_SUB_420) {
+        lo = std::max(0, lo - 1);
+        hi = std::min(rows, hi + 1);
+    }
+}
+
 }  // namespace
 
 extern "C" hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, int32_t n_threads,
@@ -839,8 +855,10 @@ extern "C" hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, i
     size_t max_coef = 0, max_rgb = 0;
     for (int i = 0; i < n; ++i) {
         const hj_stream_image_t &im = images[i];
+        const int rows_i = (im.height + mcu_h_of(im.subsampling) - 1) / mcu_h_of(im.subsampling);
         if (!im.huff || (!im.scan && im.scan_bytes) || !im.q || im.subsampling < HJ_SUB_444 ||
-            im.subsampling > HJ_SUB_420 || im.width < 1 || im.height < 1)
+            im.subsampling > HJ_SUB_420 || im.width < 1 || im.height < 1 || im.row0 < 0 || im.n_rows < 0 ||
+            im.row0 + im.n_rows > rows_i)
             return fail(HJ_ERR_ARG, "stream: image " + std::to_string(i) + ": bad descriptor");
         max_coef = std::max(max_coef, stream_coef_bytes(im));
         max_rgb = std::max(max_rgb, (size_t)im.width * im.height * 3);
@@ -919,9 +937,11 @@ extern "C" hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, i
             const int mpr = (im.width + mw - 1) / mw, rows = (im.height + mh - 1) / mh;
             const int64_t nc = (int64_t)mpr * rows, ny = nc * ypm_of(im.subsampling);
             const auto t0 = std::chrono::steady_clock::now();
-            int s = hj_decode_scan_fast(im.huff, im.scan, im.scan_bytes, sl.h_coef, sl.h_coef + ny * 64,
+            int lo, hi;
+            stream_coef_rows(im, rows, lo, hi);
+            int s = hj_decode_scan_rows(im.huff, im.scan, im.scan_bytes, sl.h_coef, sl.h_coef + ny * 64,
                                         sl.h_coef + (ny + nc) * 64, mpr, rows, ypm_of(im.subsampling),
-                                        im.restart_interval, 1);
+                                        im.restart_interval, lo, hi - lo, 1);
             huff_ns.fetch_add(std::chrono::duration_cast<std::chrono::nanoseconds>(
                                   std::chrono::steady_clock::now() - t0).count());
             (void)cb;
@@ -992,8 +1012,9 @@ extern "C" hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, i
             const int mw = mcu_w_of(src.subsampling), mh = mcu_h_of(src.subsampling);
             im.mcus_per_row = (src.width + mw - 1) / mw;
             im.mcu_rows = (src.height + mh - 1) / mh;
-            im.row0 = 0;
-            im.n_rows = im.mcu_rows;
+            const bool shard = src.n_rows > 0;
+            im.row0 = shard ? src.row0 : 0;
+            im.n_rows = shard ? src.n_rows : im.mcu_rows;
             im.subsampling = src.subsampling;
             im.flags = src.flags;
             const int64_t nc = (int64_t)im.mcus_per_row * im.mcu_rows, ny = nc * ypm_of(src.subsampling);
@@ -1021,9 +1042,22 @@ extern "C" hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, i
             std::memcpy(sl.h_plan, src.q, 768);
             std::memcpy(sl.h_plan + 1024, &im, sizeof(im));
             std::memcpy(sl.h_plan + 1024 + 256, tiles.data(), sizeof(hj::Tile) * tiles.size());
-            const size_t coef_b = (size_t)(ny + 2 * nc) * 128, rgb_b = (size_t)src.width * src.height * 3;
+            // the item's coefficient rows of each plane, and its RGB rows
+            int lo, hi;
+            stream_coef_rows(src, im.mcu_rows, lo, hi);
+            const int64_t ypr = (int64_t)im.mcus_per_row * ypm_of(src.subsampling), cpr = im.mcus_per_row;
+            const int py0 = im.row0 * mh, py1 = std::min(src.height, (im.row0 + im.n_rows) * mh);
+            const size_t rgb_off = (size_t)py0 * src.width * 3, rgb_b = (size_t)(py1 - py0) * src.width * 3;
             const size_t plan_b = 1024 + 256 + sizeof(hj::Tile) * tiles.size();
-            cudaError_t e = cudaMemcpyAsync(sl.d_coef, sl.h_coef, coef_b, cudaMemcpyHostToDevice, sl.stream);
+            size_t coef_b = 0;
+            cudaError_t e = cudaSuccess;
+            const int64_t plane_off[3] = {0, ny * 64, (ny + nc) * 64}, per_row[3] = {ypr, cpr, cpr};
+            for (int pl = 0; pl < 3 && e == cudaSuccess; ++pl) {
+                const int64_t first = plane_off[pl] + (int64_t)lo * per_row[pl] * 64;
+                const size_t bytes = (size_t)(hi - lo) * per_row[pl] * 128;
+                e = cudaMemcpyAsync(dy + first, sl.h_coef + first, bytes, cudaMemcpyHostToDevice, sl.stream);
+                coef_b += bytes;
+            }
             if (e == cudaSuccess) e = cudaMemcpyAsync(misc, sl.h_plan, plan_b, cudaMemcpyHostToDevice, sl.stream);
             for (const auto &gr : groups) {
                 if (e != cudaSuccess) break;
@@ -1037,7 +1071,8 @@ extern "C" hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, i
                 }
             }
             if (e == cudaSuccess)
-                e = cudaMemcpyAsync(src.rgb_out ? src.rgb_out : sl.h_rgb, sl.d_rgb, rgb_b, cudaMemcpyDeviceToHost,
+                e = cudaMemcpyAsync((src.rgb_out ? src.rgb_out : sl.h_rgb) + rgb_off,
+                                    static_cast<uint8_t *>(sl.d_rgb) + rgb_off, rgb_b, cudaMemcpyDeviceToHost,
                                     sl.stream);
             if (e == cudaSuccess) e = cudaEventRecord(sl.done, sl.stream);
             if (e != cudaSuccess) {

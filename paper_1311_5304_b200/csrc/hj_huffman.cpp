@@ -226,6 +226,76 @@ void hj_huff_free(void *fast) { delete static_cast<Tables *>(fast); }
 // interval's end is checked where the reference's reader would stand.  The
 // first failing interval in scan order decides the status, as in the
 // reference's sequential decode.
+}  // extern "C"
+
+namespace {
+
+// Decodes the restart intervals of a scan that overlap MCUs [m_lo, m_hi).
+// Interval boundaries are found by a byte scan from the start (each interval
+// ends where the reader stops); only the overlapping intervals are Huffman
+// decoded, on up to n_threads threads.  Without restart intervals the scan is
+// one interval and is decoded whole.
+hj_status decode_scan_mcus(const Tables *f, const uint8_t *data, int64_t n, int16_t *y, int16_t *cb, int16_t *cr,
+                           int32_t mcus_per_row, int32_t mcu_rows, int32_t y_per_mcu, int32_t restart_interval,
+                           int64_t m_lo, int64_t m_hi, int32_t n_threads) {
+    const int64_t total = (int64_t)mcus_per_row * mcu_rows;
+    m_lo = std::max<int64_t>(0, m_lo);
+    m_hi = std::min<int64_t>(total, m_hi);
+    std::vector<Segment> segs;
+    std::vector<int> expect;  // RSTn index after each segment
+    if (restart_interval <= 0 || total <= restart_interval) {
+        segs.push_back({0, 0, total, n, true});
+        expect.push_back(0);
+    } else {
+        int64_t pos = 0, mcu = 0, k = 0;
+        while (mcu < total && mcu < m_hi) {
+            const int64_t m1 = std::min<int64_t>(total, mcu + restart_interval);
+            const bool last = m1 == total;
+            const int64_t end = last ? n : stop_point(data, n, pos);
+            segs.push_back({pos, mcu, m1, end, last});
+            expect.push_back((int)(k & 7));
+            if (last) break;
+            // an interval that does not end on the expected RSTn fails its
+            // own check; nothing after it is decoded (first error wins)
+            if (check_restart(data, n, end, k & 7) != HJ_OK) break;
+            pos = end + 2;
+            mcu = m1;
+            ++k;
+        }
+    }
+    std::vector<size_t> todo;
+    for (size_t i = 0; i < segs.size(); ++i)
+        if (segs[i].mcu1 > m_lo && segs[i].mcu0 < m_hi) todo.push_back(i);
+    if (!segs.empty() && segs.back().mcu1 < m_hi && todo.empty()) todo.push_back(segs.size() - 1);
+    const int nt = std::max(1, std::min<int>(n_threads, (int)todo.size()));
+    std::atomic<int64_t> next{0};
+    std::vector<int> errs(todo.size(), HJ_OK);
+    auto work = [&]() {
+        for (int64_t t; (t = next.fetch_add(1)) < (int64_t)todo.size();) {
+            const size_t i = todo[(size_t)t];
+            errs[(size_t)t] = decode_segment(*f, data, n, segs[i], y, cb, cr, y_per_mcu, expect[i]);
+        }
+    };
+    std::vector<std::thread> th;
+    for (int i = 1; i < nt; ++i) th.emplace_back(work);
+    work();
+    for (auto &t : th) t.join();
+    for (size_t t = 0; t < errs.size(); ++t)
+        if (errs[t]) return hj::fail((hj_status)errs[t], std::string("restart interval ") + std::to_string(todo[t]) +
+                                                           ": " + status_name(errs[t]));
+    return HJ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Decode a whole scan (all MCUs; every block written, zeros included).
+// With a restart interval the intervals are located first (each one ends
+// where the reader stops), decoded on up to n_threads threads, and each
+// interval's end is checked where the reference's reader would stand.  The
+// first failing interval in scan order decides the status, as in the
+// reference's sequential decode.
 hj_status hj_decode_scan_fast(const void *fast, const uint8_t *data, int64_t n, int16_t *y, int16_t *cb,
                               int16_t *cr, int32_t mcus_per_row, int32_t mcu_rows, int32_t y_per_mcu,
                               int32_t restart_interval, int32_t n_threads) {
@@ -233,40 +303,23 @@ hj_status hj_decode_scan_fast(const void *fast, const uint8_t *data, int64_t n, 
     if (!f || (!data && n) || !y || !cb || !cr || n < 0 || mcus_per_row < 0 || mcu_rows < 0 ||
         y_per_mcu < 1 || y_per_mcu > 4)
         return hj::fail(HJ_ERR_ARG, "hj_decode_scan_fast: bad arguments");
-    const int64_t total = (int64_t)mcus_per_row * mcu_rows;
-    std::vector<Segment> segs;
-    if (restart_interval <= 0 || total <= restart_interval) {
-        segs.push_back({0, 0, total, n, true});
-    } else {
-        int64_t pos = 0, mcu = 0;
-        while (mcu < total) {
-            const int64_t m1 = std::min<int64_t>(total, mcu + restart_interval);
-            const bool last = m1 == total;
-            const int64_t end = last ? n : stop_point(data, n, pos);
-            segs.push_back({pos, mcu, m1, end, last});
-            if (last) break;
-            // an interval that does not end on the expected RSTn fails its
-            // own check; nothing after it is decoded (first error wins)
-            if (check_restart(data, n, end, (int64_t)(segs.size() - 1) & 7) != HJ_OK) break;
-            pos = end + 2;
-            mcu = m1;
-        }
-    }
-    const int nt = std::max(1, std::min<int>(n_threads, (int)segs.size()));
-    std::atomic<int64_t> next{0};
-    std::vector<int> errs(segs.size(), HJ_OK);
-    auto work = [&]() {
-        for (int64_t i; (i = next.fetch_add(1)) < (int64_t)segs.size();)
-            errs[i] = decode_segment(*f, data, n, segs[i], y, cb, cr, y_per_mcu, (int)(i & 7));
-    };
-    std::vector<std::thread> th;
-    for (int i = 1; i < nt; ++i) th.emplace_back(work);
-    work();
-    for (auto &t : th) t.join();
-    for (size_t i = 0; i < errs.size(); ++i)
-        if (errs[i]) return hj::fail((hj_status)errs[i], std::string("restart interval ") + std::to_string(i) +
-                                                           ": " + status_name(errs[i]));
-    return HJ_OK;
+    return decode_scan_mcus(f, data, n, y, cb, cr, mcus_per_row, mcu_rows, y_per_mcu, restart_interval, 0,
+                            (int64_t)mcus_per_row * mcu_rows, n_threads);
+}
+
+// MCU rows [row0, row0+n_rows) of a scan: the restart intervals covering
+// them (every block of those intervals written); a shard of a large image
+// (BASELINE config 4) decodes only its own intervals.
+hj_status hj_decode_scan_rows(const void *fast, const uint8_t *data, int64_t n, int16_t *y, int16_t *cb,
+                              int16_t *cr, int32_t mcus_per_row, int32_t mcu_rows, int32_t y_per_mcu,
+                              int32_t restart_interval, int32_t row0, int32_t n_rows, int32_t n_threads) {
+    const Tables *f = static_cast<const Tables *>(fast);
+    if (!f || (!data && n) || !y || !cb || !cr || n < 0 || mcus_per_row < 0 || mcu_rows < 0 ||
+        y_per_mcu < 1 || y_per_mcu > 4 || row0 < 0 || n_rows < 0 || row0 + n_rows > mcu_rows)
+        return hj::fail(HJ_ERR_ARG, "hj_decode_scan_rows: bad arguments");
+    if (n_rows == 0) return HJ_OK;
+    return decode_scan_mcus(f, data, n, y, cb, cr, mcus_per_row, mcu_rows, y_per_mcu, restart_interval,
+                            (int64_t)row0 * mcus_per_row, (int64_t)(row0 + n_rows) * mcus_per_row, n_threads);
 }
 
 // The drop-in cursor: MCU rows [row0, row0+n_rows) from / to the reference's

@@ -193,6 +193,24 @@ class FastScan:
         _lib.check(st, "decode_scan_fast")
         return out
 
+    def decode_rows(self, row0: int, n_rows: int, data: bytes | None = None, out: CoefficientBuffer | None = None,
+                    threads: int = 1) -> CoefficientBuffer:
+        """Only the restart intervals covering MCU rows [row0, row0+n_rows)
+        (hj_decode_scan_rows; the whole scan when it has no restart markers)."""
+        p = self.parsed
+        data = p.stream if data is None else data
+        sp = p.entropy_span
+        buf = np.frombuffer(data, dtype=np.uint8)[sp.offset:sp.offset + sp.length]
+        if out is None:
+            out = alloc_coefficients(self.geometry)
+        g = self.geometry
+        st = _lib.lib.hj_decode_scan_rows(self._h, buf.ctypes.data, len(buf), out.y_blocks.ctypes.data,
+                                          out.cb_blocks.ctypes.data, out.cr_blocks.ctypes.data, g.mcus_per_row,
+                                          g.mcu_rows, g.y_blocks_per_mcu, p.restart_interval, int(row0),
+                                          int(n_rows), int(threads))
+        _lib.check(st, "decode_scan_rows")
+        return out
+
     def __del__(self):
         if getattr(self, "_h", None):
             _lib.lib.hj_huff_free(self._h)

@@ -222,9 +222,12 @@ class StreamDecoder:
     each distinct blob is parsed and gets its Huffman tables once.  `keep`:
     indices whose RGB is copied out to page-locked arrays (self.kept[i]);
     the others are delivered into the ring and overwritten.  `order`: the
-    processing order (default: largest first, which shortens the tail)."""
+    processing order (default: largest first, which shortens the tail).
+    `shards[i]` = (row0, n_rows): decode and render only those MCU rows of
+    image i (BASELINE config 4: a rank's share of one large image; only its
+    restart intervals are Huffman-decoded)."""
 
-    def __init__(self, blobs, threads: int = 0, slots: int = 0, fast=True, keep=(), order=None):
+    def __init__(self, blobs, threads: int = 0, slots: int = 0, fast=True, keep=(), order=None, shards=None):
         import ctypes as C
         import os
 
@@ -248,6 +251,10 @@ class StreamDecoder:
         self.n = len(per)
         self.geometries = [d[2].geometry for d in per]
         self.pixels = sum(g.width * g.height for g in self.geometries)
+        if shards is not None:
+            self.pixels = sum(
+                g.width * (min(g.height, (sh[0] + sh[1]) * g.mcu_height) - sh[0] * g.mcu_height) if sh
+                else g.width * g.height for g, sh in zip(self.geometries, shards))
         if order is None:
             order = sorted(range(self.n), key=lambda i: -self.geometries[i].width * self.geometries[i].height)
         self.order = list(order)
@@ -265,6 +272,8 @@ class StreamDecoder:
             d.subsampling = device.subsampling_code(g)
             d.flags = _lib.image_flags(fast)
             d.restart_interval = p.restart_interval
+            if shards is not None and shards[i] is not None:
+                d.row0, d.n_rows = int(shards[i][0]), int(shards[i][1])
             if i in keep:
                 out = PinnedArray((g.height, g.width, 3), np.uint8)
                 self.kept[i] = out

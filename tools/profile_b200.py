@@ -4,8 +4,10 @@
 
     python tools/profile_b200.py [--out profiles/b200_profile.json] [--images 24]
 
-Training set: synthetic 4:2:0 q75-95 JPEGs (SURVEY.md Appendix B content)
-on a (w, h) grid from 256 to 2048 px; max degree 3 (10 bivariate terms).
+Training set: synthetic JPEGs (SURVEY.md Appendix B content), 4:4:4 / 4:2:2 /
+4:2:0 at q50-95, on a (w, h) grid from 320 to 6000 px - the size range of
+BASELINE config 5 (0.3-24 MP) - so the fitted degree can carry the w*h
+(area) term; max degree 3 (10 bivariate terms).
 """
 import argparse
 import json
@@ -23,18 +25,21 @@ from paper_1311_5304_b200.synth import synth_jpeg  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "b200_profile.json"))
-    ap.add_argument("--images", type=int, default=24)
+    ap.add_argument("--images", type=int, default=40)
     ap.add_argument("--repeats", type=int, default=3)
     ap.add_argument("--max-degree", type=int, default=3)
     args = ap.parse_args()
-    sizes = [256, 512, 768, 1024, 1536, 2048]
+    sizes = [320, 640, 1024, 1600, 2400, 3200, 4000, 4800, 6000]
     blobs = []
     k = 0
     while len(blobs) < args.images:
         w = sizes[k % len(sizes)]
-        h = sizes[(k * 7 + 3) % len(sizes)]
-        q = (75, 85, 95)[k % 3]
-        blobs.append(synth_jpeg(w, h, q, "420", seed=k))
+        h = sizes[(k * 4 + 3) % len(sizes)]
+        if w * h > 24.5e6:  # config 5's largest images are 24 MP
+            h = int(24e6 // w) // 16 * 16
+        q = (50, 75, 90, 95)[k % 4]
+        sub = ("420", "422", "444")[k % 3]
+        blobs.append(synth_jpeg(w, h, q, sub, seed=k))
         k += 1
     lanes = executors.make_lanes()
     t0 = time.time()
