@@ -578,6 +578,17 @@ def run_mixed(args, world, rank, local, pg):
     t_h = allreduce_max(pg, hs["wall_s"])
     t_w = allreduce_max(pg, rs["wall_s"])
     corpus_px = allreduce_sum(pg, sd.pixels)
+    # the same with one host core left to the CUDA submitter (both legs)
+    reserved = None
+    if threads > 2:
+        sd1 = pipeline.StreamDecoder([corpus[k] for k in mine], threads=threads - 1, slots=threads + 3, fast=fast)
+        barrier(pg)
+        h1 = allreduce_max(pg, sd1.huffman_only()["wall_s"])
+        barrier(pg)
+        w1 = allreduce_max(pg, sd1.run()["wall_s"])
+        reserved = {"t_huff_ms": round(h1 * 1e3, 1), "t_wall_ms": round(w1 * 1e3, 1),
+                    "frac_of_bound": round(h1 / w1, 4), "mpix_s": round(corpus_px / w1 / 1e6, 1),
+                    "host_threads_per_rank": threads - 1}
     exact = True
     for j, k in enumerate(keep[:len(sd.kept)]):
         b = corpus[k]
@@ -615,7 +626,8 @@ def run_mixed(args, world, rank, local, pg):
             "amdahl": {"t_huff_ms": round(t_h * 1e3, 1), "t_wall_ms": round(t_w * 1e3, 1),
                        "frac_of_bound": round(t_h / t_w, 4), "mpix_s": round(corpus_px / t_w / 1e6, 1),
                        "huffman_mpix_s": round(corpus_px / t_h / 1e6, 1), "host_threads_per_rank": threads,
-                       "images": len(man),
+                       "images": len(man), "one_core_reserved": reserved,
+                       "setup_s_excluded": round(rs["call_s"] - rs["wall_s"], 2),
                        "memory": {"ring_pinned_bytes_per_rank": int(ring),
                                   "ring_device_bytes_per_rank": int(rs["device_bytes"]),
                                   "peak_rss_gb_per_rank": round(peak_rss, 2)}},

@@ -245,6 +245,33 @@ hj_status hj_pipeline_run(const hj_pipe_image_t *images, int32_t n_images, int32
 /* The same host stage alone (T_huff of the Amdahl bound, orchestrator.py:71-75). */
 hj_status hj_pipeline_huffman(const hj_pipe_image_t *images, int32_t n_images, int32_t n_threads);
 
+/* ---- host/accelerator row split (partitioner, Eq. 10-15) -----
+ * A balance f(x) = sum_i sign_i * P_i(a_i), P_i an ascending univariate
+ * polynomial (the DeviceProfile's models restricted to the image width; a
+ * constant is a 1-coefficient polynomial) and a_i = x (host rows) or h - x
+ * (accelerator rows, `reflected`).  hj_partition_solve finds its root on
+ * [0, h] (Newton on the analytic derivative, bisection fallback; the
+ * iteration limits and tolerances of partitioner.py:95-135) and rounds the
+ * accelerator share to whole MCU rows from the top (partitioner.py:138-155).
+ * Replaces partitioner._solve_balance / _to_plan. */
+typedef struct {
+    const double *coef;
+    int32_t n;          /* coefficients, ascending powers */
+    int32_t reflected;  /* evaluate at h - x */
+    double sign;        /* +1 or -1 */
+} hj_balance_term_t;
+
+typedef struct {
+    double x_root;                      /* host rows before rounding */
+    int32_t accel_mcu_rows, cpu_mcu_rows;
+    int32_t accel_rows, cpu_rows;       /* pixel rows */
+} hj_partition_t;
+
+hj_status hj_partition_solve(const hj_balance_term_t *terms, int32_t n_terms, int32_t h, int32_t mcu_height,
+                             hj_partition_t *out);
+/* f(x) (and f'(x) in *slope when non-NULL) of a balance - tests and diagnostics. */
+double hj_balance_eval(const hj_balance_term_t *terms, int32_t n_terms, double h, double x, double *slope);
+
 /* ---- streaming decode with a bounded ring (BASELINE config 5) ---------
  * One image of a stream: its scan (hj_huff_build tables + entropy-coded
  * bytes), its host qtables and its geometry.  rgb_out: host destination of
@@ -270,6 +297,7 @@ typedef struct {
     int64_t h2d_bytes, d2h_bytes;         /* moved by the GPU leg */
     int64_t pinned_bytes, device_bytes;   /* the ring's whole footprint */
     double huffman_thread_s;              /* summed host entropy-decode time */
+    double wall_s;                        /* first image taken -> last RGB delivered (ring set-up excluded) */
 } hj_stream_stats_t;
 
 /* Decode n images in list order with n_slots reusable slots (page-locked

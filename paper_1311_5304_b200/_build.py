@@ -18,12 +18,12 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhetjpeg_b200.so")
-SOURCES = ["hj_render.cu", "hj_blockops.cu", "hj_api.cu", "hj_huffman.cpp"]
+SOURCES = ["hj_render.cu", "hj_blockops.cu", "hj_api.cu", "hj_huffman.cpp", "hj_sched.cpp"]
 HEADERS = ["hj_render.cuh", "hj_common.cuh", "hj_screen.h", "hj_tables.h", "hj_huffman.h", "hj_error.h",
            os.path.join("..", "..", "include", "hetjpeg_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off", "-shared",
          "-Xptxas", "-warn-spills"]
 
 

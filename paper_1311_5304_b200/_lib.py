@@ -103,7 +103,17 @@ class hj_stream_stats_t(C.Structure):  # noqa: N801
     _fields_ = [
         ("images", C.c_int64), ("launches", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
         ("pinned_bytes", C.c_int64), ("device_bytes", C.c_int64), ("huffman_thread_s", C.c_double),
+        ("wall_s", C.c_double),
     ]
+
+
+class hj_balance_term_t(C.Structure):  # noqa: N801
+    _fields_ = [("coef", C.c_void_p), ("n", C.c_int32), ("reflected", C.c_int32), ("sign", C.c_double)]
+
+
+class hj_partition_t(C.Structure):  # noqa: N801
+    _fields_ = [("x_root", C.c_double), ("accel_mcu_rows", C.c_int32), ("cpu_mcu_rows", C.c_int32),
+                ("accel_rows", C.c_int32), ("cpu_rows", C.c_int32)]
 
 
 if not os.path.exists(_LIB_PATH):
@@ -159,6 +169,9 @@ _SIG = {
     "hj_decode_scan_fast": (C.c_int, [_P, _P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _I32]),
     "hj_decode_scan_rows": (C.c_int, [_P, _P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32]),
     "hj_pipeline_run": (C.c_int, [C.POINTER(hj_pipe_image_t), _I32, _I32, C.POINTER(_P)]),
+    "hj_partition_solve": (C.c_int, [C.POINTER(hj_balance_term_t), _I32, _I32, _I32, C.POINTER(hj_partition_t)]),
+    "hj_balance_eval": (C.c_double, [C.POINTER(hj_balance_term_t), _I32, C.c_double, C.c_double,
+                                     C.POINTER(C.c_double)]),
     "hj_stream_run": (C.c_int, [C.POINTER(hj_stream_image_t), _I32, _I32, _I32, _I32,
                                 C.POINTER(hj_stream_stats_t)]),
     "hj_pipeline_huffman": (C.c_int, [C.POINTER(hj_pipe_image_t), _I32, _I32]),

@@ -960,6 +960,7 @@ extern "C" hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, i
             cv_ready.notify_one();
         }
     };
+    const auto t_start = std::chrono::steady_clock::now();  // slots are allocated: the decode proper
     std::vector<std::thread> pool;
     for (int t = 0; t < n_threads; ++t) pool.emplace_back(worker);
 
@@ -1104,6 +1105,7 @@ extern "C" hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, i
     }
     while (!inflight.empty()) recycle(true);
     for (auto &th : pool) th.join();
+    st.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     st.huffman_thread_s = (double)huff_ns.load() * 1e-9;
     if (!gpu) st.images = n;
     release();

@@ -1044,7 +1044,8 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
         __syncthreads();
 
         // ---------------- phase B: exact recompute of this step's queue ...
-        {
+        // (the islow mode is exact integer arithmetic: nothing is ever queued)
+        if constexpr (!kIslow) {
             const int n = *nq;
             const int grp = tid >> 3, l = tid & 7;
             const unsigned gmask = 0xffu << (tid & 24);  // the 8 lanes of this group

@@ -287,8 +287,8 @@ class StreamDecoder:
         t0 = time.perf_counter()
         _lib.check(_lib.lib.hj_stream_run(self._arr, self.n, self.threads, self.slots, gpu,
                                           self._C.byref(stats)), "hj_stream_run")
-        wall = time.perf_counter() - t0
-        return {"wall_s": wall, "images": stats.images, "launches": stats.launches,
+        call = time.perf_counter() - t0
+        return {"wall_s": stats.wall_s, "call_s": call, "images": stats.images, "launches": stats.launches,
                 "h2d_bytes": stats.h2d_bytes, "d2h_bytes": stats.d2h_bytes,
                 "pinned_bytes": stats.pinned_bytes, "device_bytes": stats.device_bytes,
                 "huffman_thread_s": stats.huffman_thread_s}
