@@ -342,6 +342,41 @@ def amdahl_run(images, wl, world, pg, n_images, reserve=0, idct="fast"):
                     "stream; medians of 7 interleaved runs, max over ranks"}
 
 
+def amdahl_rows(images, wl, world, pg, n_images, row0, n_rows, idct):
+    """--shard rows (BASELINE config 4): every rank decodes ITS MCU-row shard
+    of each image - Huffman of only the restart intervals covering it
+    (hj_decode_scan_rows) pipelined with H2D / render / D2H of its rows
+    through the streaming ring - against that Huffman stage alone."""
+    from paper_1311_5304_b200 import pipeline
+    threads = max(1, len(os.sched_getaffinity(0)) // world)
+    blobs = [images[i % len(images)][0] for i in range(n_images)]
+    sd = pipeline.StreamDecoder(blobs, threads=threads, slots=threads + 2, fast=idct_arg_s(idct),
+                                keep=(0,), shards=[(row0, n_rows)] * n_images)
+    sd.huffman_only()
+    barrier(pg)
+    hs = sd.huffman_only()
+    barrier(pg)
+    rs = sd.run()
+    t_h = allreduce_max(pg, hs["wall_s"])
+    t_w = allreduce_max(pg, rs["wall_s"])
+    _, _, c0, q0 = images[0]
+    w, h = wl[0], wl[1]
+    mh = c0.geometry.mcu_height
+    want = oracle_render(c0, q0, w, h, {"444": 0, "422": 1, "420": 2}[wl[3]], idct, threads)
+    y0, y1 = row0 * mh, min(h, (row0 + n_rows) * mh)
+    exact = bool(np.array_equal(sd.rgb(0)[y0:y1], want[y0:y1]))
+    px = allreduce_sum(pg, sd.pixels)
+    return {"t_huff_ms": round(t_h * 1e3, 3), "t_wall_ms": round(t_w * 1e3, 3), "frac_of_bound": round(t_h / t_w, 4),
+            "mpix_s": round(px / t_w / 1e6, 1), "huffman_mpix_s": round(px / t_h / 1e6, 1),
+            "host_threads_per_rank": threads, "images_per_rank": n_images, "bit_exact_vs_oracle": exact,
+            "note": "each rank Huffman-decodes only the restart intervals of its MCU-row shard "
+                    "(hj_decode_scan_rows) and streams them through hj_stream_run; max over ranks"}
+
+
+def idct_arg_s(idct):
+    return {"fast": True, "direct": False, "islow": "islow"}[idct]
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as fh:
@@ -845,7 +880,9 @@ def main():
 
     # ---- end to end INCLUDING host Huffman: the paper's Amdahl metric
     amdahl = None
-    if not args.no_amdahl:
+    if not args.no_amdahl and rows_mode:
+        amdahl = amdahl_rows(images, wl, world, pg, args.amdahl_images, row0, n_rows, args.idct)
+    elif not args.no_amdahl:
         amdahl = amdahl_run(images, wl, world, pg, args.amdahl_images, idct=args.idct)
         # the same with one host core left to the GPU submission thread and
         # the driver (both legs on the remaining cores): all-cores Huffman
