@@ -532,6 +532,13 @@ struct Geo<HJ_SUB_420> {
 #ifndef HJ_CSTAGE
 #define HJ_CSTAGE 1
 #endif
+// timing ablations (tools/ablate.sh; wrong bytes): no IDCT screen / no pixel stage
+#ifndef HJ_ABLATE_SCREEN
+#define HJ_ABLATE_SCREEN 0
+#endif
+#ifndef HJ_ABLATE_PIXELS
+#define HJ_ABLATE_PIXELS 0
+#endif
 #ifndef HJ_PF_L2
 #define HJ_PF_L2 1
 #endif
@@ -988,6 +995,15 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     if constexpr (kIslow) {
                         islow_block(k ? srcB : srcA, sm.qi[comp], w);
                         ok = true;
+                    } else if (HJ_ABLATE_SCREEN) {
+                        // timing ablation only (wrong bytes): load the block, no transform
+                        int4 r[8];
+#pragma unroll
+                        for (int i = 0; i < 8; i += 2)
+                            ldg_rows2(reinterpret_cast<const int4 *>(k ? srcB : srcA) + i, r[i], r[i + 1]);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) w[i] = (uint32_t)(r[i >> 1].x ^ r[i >> 1].w) + i;
+                        ok = true;
                     } else if (!direct) {
                         ok = screen_block<SUB>(k ? srcB : srcA, sm.qf[comp], w);
                     }
@@ -1071,7 +1087,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
 
         // ---------------- ... overlapped with the pixel stage of MCU row s-1
         const int R = s - 1;
-        if (R >= t.r0 && R < t.r1) {
+        if (!HJ_ABLATE_PIXELS && R >= t.r0 && R < t.r1) {
             const int y_base = R * G::MH;
             const int x_base = t.m0 * G::MW;
             const uint8_t *yp = sm.ys[par ^ 1];
