@@ -193,14 +193,15 @@ def check(status: int, what: str = "") -> None:
     if status == HJ_OK:
         return
     msg = last_error() or what
-    if status == HJ_ERR_EXHAUSTED:
-        raise BitstreamExhausted("ran out of entropy-coded bits")
-    if status == HJ_ERR_BADCODE:
-        raise BadCode("no Huffman symbol matches within 16 bits")
-    if status == HJ_ERR_MARKER:
-        raise MarkerInScan("non-restart marker inside the scan")
-    if status == HJ_ERR_RST_SEQ:
-        raise MarkerInScan("restart marker out of sequence")
+    # entropy errors carry the reference's messages (_native.pyx:298-305); the
+    # library's context (which image / restart interval) is appended when it has one
+    ref = {HJ_ERR_EXHAUSTED: (BitstreamExhausted, "ran out of entropy-coded bits"),
+           HJ_ERR_BADCODE: (BadCode, "no Huffman symbol matches within 16 bits"),
+           HJ_ERR_MARKER: (MarkerInScan, "non-restart marker inside the scan"),
+           HJ_ERR_RST_SEQ: (MarkerInScan, "restart marker out of sequence")}.get(status)
+    if ref is not None:
+        cls, text = ref
+        raise cls(text if not msg or msg == text else f"{text} ({msg})")
     if status == HJ_ERR_ARG:
         raise ValueError(msg)
     if status == HJ_ERR_NODEVICE:

@@ -97,3 +97,20 @@ def test_stream_gpu_bit_exact_and_shards():
     for k, (r0, n) in enumerate(shards):
         y0, y1 = r0 * 16, min(g.height, (r0 + n) * 16)
         assert np.array_equal(sd.rgb(k)[y0:y1], want[y0:y1]), (r0, n)
+
+
+def test_stream_reports_the_first_failing_image():
+    from paper_1311_5304_b200 import errors, parser, pipeline
+    from paper_1311_5304_b200.synth import synth_jpeg
+    good = synth_jpeg(200, 120, 80, "422", seed=1)
+    p = parser.parse_stream(good)
+    sp = p.entropy_span
+    bad = bytearray(good)
+    # scramble the middle of the scan: a Huffman error or an early stop
+    mid = sp.offset + sp.length // 2
+    bad[mid:mid + 40] = bytes([0xFF, 0xD9]) * 20
+    bad = bytes(bad)
+    sd = pipeline.StreamDecoder([good, good, bad, good], threads=2, slots=2, order=[0, 1, 2, 3])
+    with pytest.raises((errors.BitstreamExhausted, errors.BadCode, errors.MarkerInScan)) as ei:
+        sd.huffman_only()
+    assert "image 2" in str(ei.value)
