@@ -122,6 +122,10 @@ uint64_t hj_launch_count(void);
  * in exact float64 (cumulative, all launches). */
 uint64_t hj_exact_block_count(void);
 
+/* Launches of the tensor-core IDCT-screen kernel (opt-in with HJ_RENDER_TC=1 in
+ * the environment), cumulative since library load. */
+uint64_t hj_tc_launch_count(void);
+
 /* ---- the parallel phase: synchronous host-buffer drop-in -------------- */
 /* Exactly the backend contract of render_rows_444 / render_rows_422
  * (kernels/_native.pyx:532-549, kernels/fallback.py:224-260): HOST arrays,

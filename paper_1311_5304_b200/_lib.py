@@ -153,6 +153,7 @@ _SIG = {
     "hj_plan_destroy": (C.c_int, [_P]),
     "hj_launch_count": (C.c_uint64, []),
     "hj_exact_block_count": (C.c_uint64, []),
+    "hj_tc_launch_count": (C.c_uint64, []),
     "hj_render_rows": (C.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
                                  _I32, _I32, _I64, _I64]),
     "hj_render_rows_timed": (C.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32,

@@ -91,7 +91,7 @@ struct Plan {
     size_t bytes = 0;
     size_t tile_base = 0;  // byte offset of the Tile array in dev
     int n_images = 0;
-    // kind: 0 AAN, 1 direct basis (both the reference's float64 mode), 2 islow
+    // kind: hj::kKind* (tensor-core AAN, direct basis, islow, FP32-screen AAN)
     struct Group { int sub; int kind; int offset; int count; };
     std::vector<Group> groups;
     // a batch mixing subsamplings launches one kernel per family; they are
@@ -122,10 +122,22 @@ static int64_t strips_of(int mpr, int S, int sub) {
     return (mpr + S - 1) / S;
 }
 
-// Launch group of an image: the float64 AAN (0) / direct (1) paths share a
-// kernel but keep separate tiles (their costs differ); islow (2) has its own.
+// Launch group of an image: the float64 AAN path runs on the FP32-screen
+// kernel (kKindSimt, v3) - or, with HJ_RENDER_TC=1 in the environment, on the
+// tensor-core screen kernel (kKindTc, v4: bit-exact, 0.54x the v3 rate on
+// the B200); direct (kKindDirect) and islow (kKindIslow)
+// have their own groups.
+static bool tc_enabled() {
+    static const bool on = [] {
+        const char *v = std::getenv("HJ_RENDER_TC");
+        return v && v[0] && v[0] != '0';
+    }();
+    return on;
+}
 static int idct_kind(const hj_image_t &im) {
-    return (im.flags & HJ_FLAG_ISLOW_IDCT) ? 2 : (im.flags & HJ_FLAG_DIRECT_IDCT) ? 1 : 0;
+    if (im.flags & HJ_FLAG_ISLOW_IDCT) return hj::kKindIslow;
+    if (im.flags & HJ_FLAG_DIRECT_IDCT) return hj::kKindDirect;
+    return tc_enabled() ? hj::kKindTc : hj::kKindSimt;
 }
 
 int choose_rows_per_tile(const hj_image_t *images, int n, int sub, int kind, int S, int64_t slots) {
@@ -158,9 +170,10 @@ void build_tiles(const hj_image_t *images, int n, std::vector<hj::Tile> &tiles,
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     for (int sub = HJ_SUB_444; sub <= HJ_SUB_420; ++sub) {
-        const int64_t slots = (int64_t)sms * hj::ctas_per_sm(sub);  // resident CTAs
-        for (int kind = 0; kind < 3; ++kind) {
-            int S = hj::strip_width(sub);
+        for (int kind = 0; kind < 4; ++kind) {
+            const bool tcg = kind == hj::kKindTc;
+            const int64_t slots = (int64_t)sms * (tcg ? hj::kTcCtasPerSm : hj::ctas_per_sm(sub));  // resident CTAs
+            int S = tcg ? hj::tc_strip(sub) : hj::strip_width(sub);
             int64_t strip_rows = 0, strips = 0;
             for (;;) {
                 strip_rows = strips = 0;
@@ -267,7 +280,7 @@ hj_status plan_launch(const Plan *p, cudaStream_t stream) {
         const auto &g = p->groups[k];
         cudaStream_t st = k == 0 ? stream : p->side[k - 1];
         cudaError_t e = k > 0 ? cudaStreamWaitEvent(st, p->ev[0], 0) : cudaSuccess;
-        if (e == cudaSuccess) e = hj::launch_render(g.sub, g.kind == 2 ? hj::kModeIslow : hj::kModeRef, imgs, tiles + g.offset, g.count, st);
+        if (e == cudaSuccess) e = hj::launch_render(g.sub, hj::mode_of_kind(g.kind), imgs, tiles + g.offset, g.count, st);
         if (e != cudaSuccess) {
             st_out = cuda_fail(e, "render kernel launch");
             break;
@@ -604,6 +617,7 @@ hj_status hj_pipeline_huffman(const hj_pipe_image_t *images, int32_t n_images, i
 }
 
 uint64_t hj_exact_block_count(void) { return hj::exact_block_count(); }
+uint64_t hj_tc_launch_count(void) { return hj::tc_launch_count(); }
 
 static hj_status render_rows_impl(const int16_t *y, const int16_t *cb, const int16_t *cr,
                                   const int32_t *q3x64, uint8_t *rgb, int32_t width, int32_t height,
@@ -681,7 +695,7 @@ static hj_status render_rows_impl(const int16_t *y, const int16_t *cb, const int
     const hj_image_t *dimg = reinterpret_cast<const hj_image_t *>(misc + img_off);
     const hj::Tile *dtiles = reinterpret_cast<const hj::Tile *>(misc + tile_off);
     for (const auto &g : groups) {
-        cudaError_t e = hj::launch_render(g.sub, g.kind == 2 ? hj::kModeIslow : hj::kModeRef, dimg, dtiles + g.offset, g.count, c->stream);
+        cudaError_t e = hj::launch_render(g.sub, hj::mode_of_kind(g.kind), dimg, dtiles + g.offset, g.count, c->stream);
         if (e != cudaSuccess) return cuda_fail(e, "render kernel launch");
         g_launches.fetch_add(1, std::memory_order_relaxed);
     }
@@ -1062,7 +1076,7 @@ extern "C" hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, i
             if (e == cudaSuccess) e = cudaMemcpyAsync(misc, sl.h_plan, plan_b, cudaMemcpyHostToDevice, sl.stream);
             for (const auto &gr : groups) {
                 if (e != cudaSuccess) break;
-                e = hj::launch_render(gr.sub, gr.kind == 2 ? hj::kModeIslow : hj::kModeRef,
+                e = hj::launch_render(gr.sub, hj::mode_of_kind(gr.kind),
                                       reinterpret_cast<const hj_image_t *>(misc + 1024),
                                       reinterpret_cast<const hj::Tile *>(misc + 1024 + 256) + gr.offset, gr.count,
                                       sl.stream);

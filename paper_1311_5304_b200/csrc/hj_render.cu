@@ -39,6 +39,8 @@
 #include "hj_common.cuh"
 #include "hj_render.cuh"
 #include "hj_screen.h"
+#include "hj_mtable.h"
+#include "hj_tc.cuh"
 
 namespace hj {
 
@@ -502,32 +504,34 @@ __device__ __noinline__ uint2 exact_block_x8(const int16_t *__restrict__ src, co
 // planes per 32-bit op; 4:2:0 scales by 16 and 4:2:2 by 64 so the filtered
 // values land in byte 1 / byte 3 of each word (every lane stays below 2^16).
 // The 4:2:x chroma window covers MCUs [m0-1, m1+1).
-template <int SUB>
-struct Geo;
-template <>
-struct Geo<HJ_SUB_444> {
-    static constexpr int S = kStrip444, MW = 8, MH = 8;
+template <int SUB, int S_>
+struct GeoT;
+template <int S_>
+struct GeoT<HJ_SUB_444, S_> {
+    static constexpr int S = S_, MW = 8, MH = 8;
     static constexpr int YW = 8 * S;      // Y / Cb / Cr plane width (bytes)
     static constexpr int CW = 0;
     static constexpr int YSLOTS = 2;
     static constexpr int CROWS = 0;
 };
-template <>
-struct Geo<HJ_SUB_422> {
-    static constexpr int S = kStrip422, MW = 16, MH = 8, CSH = 6;
+template <int S_>
+struct GeoT<HJ_SUB_422, S_> {
+    static constexpr int S = S_, MW = 16, MH = 8, CSH = 6;
     static constexpr int YW = 16 * S;
     static constexpr int CW = 8 * (S + 2);  // SWAR window width (words)
     static constexpr int YSLOTS = 2;
     static constexpr int CROWS = 2 * 8;     // two slots of one MCU row
 };
-template <>
-struct Geo<HJ_SUB_420> {
-    static constexpr int S = kStrip420, MW = 16, MH = 16, CSH = 4;
+template <int S_>
+struct GeoT<HJ_SUB_420, S_> {
+    static constexpr int S = S_, MW = 16, MH = 16, CSH = 4;
     static constexpr int YW = 16 * S;
     static constexpr int CW = 8 * (S + 2);
     static constexpr int YSLOTS = 2;
     static constexpr int CROWS = 3 * 8 + 1;  // three MCU-row slots + the saved last row (index 24)
 };
+template <int SUB>
+using Geo = GeoT<SUB, SUB == HJ_SUB_444 ? kStrip444 : SUB == HJ_SUB_422 ? kStrip422 : kStrip420>;
 
 #ifndef HJ_CSTAGE
 #define HJ_CSTAGE 1
@@ -854,6 +858,176 @@ __device__ __forceinline__ void lj_right_edge(uint32_t (&c)[10], int cw, int c0)
         if (t == j) c[t + 1] = c[t];
 }
 
+// Phase B, first half: the step's queued blocks recomputed in exact float64
+// by 8-thread groups (NT / 8 blocks in parallel), written over the screen's
+// samples in the planes.  The islow mode never queues.
+template <int SUB, int MODE, class G, int NT, class SM>
+__device__ __forceinline__ void exact_phase(SM &sm, uint8_t *smem_raw, const hj_image_t &im, int par, bool direct) {
+    constexpr bool kIslow = MODE == kModeIslow;
+    constexpr int kExactGroups = NT / 8;
+    const int tid = threadIdx.x;
+    int *const nq = &sm.n_queue[par];
+    const uint32_t *const queue = sm.queue[par];
+    const uint32_t *const qdst = sm.qdst[par];
+    if constexpr (!kIslow) {
+        const int n = *nq;
+        const int grp = tid >> 3, l = tid & 7;
+        const unsigned gmask = 0xffu << (tid & 24);  // the 8 lanes of this group
+#pragma unroll 1
+        for (int e = grp; e < n; e += kExactGroups) {
+            const uint32_t job = queue[e], dst = qdst[e];
+            const int comp = job >> 30;
+            const int64_t blk = job & 0x3fffffff;
+            const int16_t *src = (comp == 0 ? im.y : comp == 1 ? im.cb : im.cr) + blk * 64;
+            const uint2 row = exact_block_x8(src, sm.qi[comp], direct, sm.g[grp], l, gmask);
+            const uint32_t kind = dst >> 30, off = dst & 0x3fffffff;
+            if (kind == 0) {
+                *reinterpret_cast<uint2 *>(smem_raw + off + l * G::YW) = row;
+            } else if constexpr (SUB != HJ_SUB_444) {
+                uint8_t *c8 = reinterpret_cast<uint8_t *>(&sm.cs[0][0] + off + l * G::CW) + (kind & 1);
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    c8[2 * c] = (uint8_t)(c < 4 ? row.x >> (8 * c) : row.y >> (8 * (c - 4)));
+            }
+        }
+        if (tid == 0 && n) atomicAdd(&g_exact_blocks, (unsigned long long)n);
+    }
+
+}
+
+// Phase B, second half: the pixel stage of MCU row R = s - 1 (upsample +
+// colour + RGB stores) from the previous step's sample planes; items are
+// handed out through a shared counter so threads busy in exact_phase take fewer.
+template <int SUB, int MODE, class G, class SM>
+__device__ __forceinline__ void pixel_phase(SM &sm, const hj_image_t &im, const Tile &t, int s, int par, bool do_c) {
+    constexpr bool kIslow = MODE == kModeIslow;
+    const int tid = threadIdx.x;
+    const int mpr = im.mcus_per_row, mcu_rows = im.mcu_rows, S = t.m1 - t.m0;
+    const bool left_edge = (t.m0 == 0), right_edge = (t.m1 == mpr);
+    const int lj_cw = (im.width + 1) >> 1, lj_ch = (im.height + 1) >> 1;
+    const bool lj_box = kIslow && lj_cw <= 2;
+    (void)lj_ch; (void)lj_cw; (void)mcu_rows; (void)tid; (void)do_c;
+    const int R = s - 1;
+    if (!HJ_ABLATE_PIXELS && R >= t.r0 && R < t.r1) {
+        const int y_base = R * G::MH;
+        const int x_base = t.m0 * G::MW;
+        const uint8_t *yp = sm.ys[par ^ 1];
+        int *const taken = &sm.n_taken[par];
+        if constexpr (SUB == HJ_SUB_420) {
+            // item = (MCU column g, row pair p): output rows y_base+2p, +1
+            const int n_items = 8 * S;
+            const int gw = S;
+            const float inv_w = 1.0f / (float)gw;
+            const uint16_t *cnear = &sm.cs[0][0] + (R % 3) * 8 * G::CW;
+            const uint16_t *cnext = &sm.cs[0][0] + ((R + 1) % 3) * 8 * G::CW;
+            // top context of the MCU row's first sample row: the last row
+            // of MCU row R-1 - saved in row 24 when this step's chroma
+            // jobs overwrote its slot, else still in the slot
+            const uint16_t *cprev = do_c ? &sm.cs[24][0] : &sm.cs[0][0] + (((R + 2) % 3) * 8 + 7) * G::CW;
+#pragma unroll 1
+            for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
+                const int i = i0;
+                if (i >= n_items) continue;
+                // row-major items: adjacent lanes store adjacent 48-byte runs
+                const int p = __float2int_rd(((float)i + 0.5f) * inv_w), g = i - p * S;
+                const int y0 = y_base + 2 * p;
+                if (y0 >= im.height) continue;
+                const int x0 = x_base + 16 * g;
+                const int npx = min(16, im.width - x0);
+                if (npx <= 0) continue;
+                const int kw = 8 * (g + 1);  // window word of the MCU's chroma column 0
+                const uint16_t *pn = cnear + p * G::CW + kw;
+                const uint16_t *pu = p > 0 ? pn - G::CW : (R > 0 ? cprev + kw : pn);
+                const uint16_t *pd = p < 7 ? pn + G::CW : (R + 1 < mcu_rows ? cnext + kw : pn);
+                if (kIslow) {
+                    // libjpeg context rows: the real chroma plane ends at row
+                    // ceil(h/2) - 1 (jdmainct.c set_bottom_pointers); box
+                    // replication has no vertical filter
+                    if (lj_box || 8 * R + p >= lj_ch - 1) pd = pn;
+                    if (lj_box) pu = pn;
+                }
+                const bool le = left_edge && g == 0, re = right_edge && g == S - 1;
+                const int c0 = 8 * (t.m0 + g);  // the item's first chroma column
+                // colsum = 3*near + far per lane (libjpeg h2v2 fancy), 16x scaled
+                uint32_t n3[10];
+                load_c10(pn, le, re, n3);
+                if (kIslow && c0 + 8 >= lj_cw) lj_right_edge(n3, lj_cw, c0);
+#pragma unroll
+                for (int k = 0; k < 10; ++k) n3[k] = n3[k] * (3u << G::CSH) + 0x00200020u;
+                const int rows = min(2, im.height - y0);
+#pragma unroll 1
+                for (int h = 0; h < rows; ++h) {
+                    uint32_t cs10[10];
+                    load_c10(h ? pd : pu, le, re, cs10);
+                    if (kIslow && c0 + 8 >= lj_cw) lj_right_edge(cs10, lj_cw, c0);
+#pragma unroll
+                    for (int k = 0; k < 10; ++k) cs10[k] = (cs10[k] << G::CSH) + n3[k];
+                    // even 16(3cs+prev+8), odd 16(3cs+next+7): each colsum
+                    // carries +2 (x16) from n3, so 3cs+prev already holds
+                    // the +8 and odd subtracts 1 (lanes stay >= 0x80)
+                    uint8_t *dst = im.rgb + ((int64_t)(y0 + h) * im.width + x0) * 3;
+                    const uint4 yv = lds128(yp + (2 * p + h) * G::YW + 16 * g);
+                    if (kIslow && lj_box)
+                        render16_swar<MODE, true>(dst, yv, cs10, 0u, 0u - 0x00100010u, npx);
+                    else
+                        render16_swar<MODE>(dst, yv, cs10, 0u, 0u - 0x00100010u, npx);
+                }
+            }
+        } else if constexpr (SUB == HJ_SUB_422) {
+            // item = (MCU column g, row y): 16 pixels
+            const int n_items = 8 * S;
+            const int gw = S;
+            const float inv_w = 1.0f / (float)gw;
+            const uint16_t *crow0 = &sm.cs[0][0] + (par ^ 1) * 8 * G::CW;
+#pragma unroll 1
+            for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
+                const int i = i0;
+                if (i >= n_items) continue;
+                const int y = __float2int_rd(((float)i + 0.5f) * inv_w), g = i - y * gw;
+                const int yy = y_base + y;
+                if (yy >= im.height) continue;
+                const int x0 = x_base + 16 * g;
+                const int npx = min(16, im.width - x0);
+                if (npx <= 0) continue;
+                uint32_t c10[10];
+                load_c10(crow0 + y * G::CW + 8 * (g + 1), left_edge && g == 0, right_edge && g == S - 1, c10);
+                const int c0 = 8 * (t.m0 + g);
+                if (kIslow && c0 + 8 >= lj_cw) lj_right_edge(c10, lj_cw, c0);
+#pragma unroll
+                for (int k = 0; k < 10; ++k) c10[k] = (c10[k] << G::CSH) + 0x00100010u;
+                // h2v1 on 64x-scaled lanes: even 64(3c+prev+1), odd 64(3c+next+2);
+                // each sample carries +1/4 (x64), so 3c+prev already holds the +1
+                uint8_t *dst = im.rgb + ((int64_t)yy * im.width + x0) * 3;
+                const uint4 yv = lds128(yp + y * G::YW + 16 * g);
+                if (kIslow && lj_box)
+                    render16_swar<MODE, true>(dst, yv, c10, 0u, 0x00400040u, npx);
+                else
+                    render16_swar<MODE>(dst, yv, c10, 0u, 0x00400040u, npx);
+            }
+        } else {
+            // item = (MCU pair g, row y): 16 pixels
+            const int gw = (S + 1) / 2;
+            const int n_items = 8 * gw;
+            const float inv_w = 1.0f / (float)gw;
+            const uint8_t *cbp = sm.cbp[par ^ 1], *crp = sm.crp[par ^ 1];
+#pragma unroll 1
+            for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
+                const int i = i0;
+                if (i >= n_items) continue;
+                const int y = __float2int_rd(((float)i + 0.5f) * inv_w), g = i - y * gw;
+                const int yy = y_base + y;
+                if (yy >= im.height) continue;
+                const int x0 = x_base + 16 * g;
+                const int npx = min(min(16, im.width - x0), 8 * (S - 2 * g));
+                if (npx <= 0) continue;
+                const int o = y * G::YW + 16 * g;
+                render16_444<MODE>(im.rgb + ((int64_t)yy * im.width + x0) * 3, lds128(yp + o), lds128(cbp + o),
+                             lds128(crp + o), npx);
+            }
+        }
+    }
+}
+
 template <int SUB, int MODE>
 __global__ void __launch_bounds__(kNT<SUB>, ctas_per_sm(SUB))
 render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ tiles) {
@@ -1060,153 +1234,475 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
         __syncthreads();
 
         // ---------------- phase B: exact recompute of this step's queue ...
-        // (the islow mode is exact integer arithmetic: nothing is ever queued)
-        if constexpr (!kIslow) {
-            const int n = *nq;
-            const int grp = tid >> 3, l = tid & 7;
-            const unsigned gmask = 0xffu << (tid & 24);  // the 8 lanes of this group
-#pragma unroll 1
-            for (int e = grp; e < n; e += kExactGroups) {
-                const uint32_t job = queue[e], dst = qdst[e];
-                const int comp = job >> 30;
-                const int64_t blk = job & 0x3fffffff;
-                const int16_t *src = (comp == 0 ? im.y : comp == 1 ? im.cb : im.cr) + blk * 64;
-                const uint2 row = exact_block_x8(src, sm.qi[comp], direct, sm.g[grp], l, gmask);
-                const uint32_t kind = dst >> 30, off = dst & 0x3fffffff;
-                if (kind == 0) {
-                    *reinterpret_cast<uint2 *>(smem_raw + off + l * G::YW) = row;
-                } else if constexpr (SUB != HJ_SUB_444) {
-                    uint8_t *c8 = reinterpret_cast<uint8_t *>(&sm.cs[0][0] + off + l * G::CW) + (kind & 1);
+        exact_phase<SUB, MODE, G, kThreads>(sm, smem_raw, im, par, direct);
+        // ---------------- ... overlapped with the pixel stage of MCU row s-1
+        pixel_phase<SUB, MODE, G>(sm, im, t, s, par, do_c);
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------ tensor-core IDCT screen (v4)
+// The reference mode's IDCT is a fixed linear map: with
+// exact arithmetic, s = M x for the dequantised block x, M evaluated exactly
+// from the reference's float64 constants (tools/gen_mtable.py).  The screen
+// computes s on the 5th-generation tensor cores in exact integer arithmetic:
+//   A = the AC coefficients as int8 (the low byte of each int16; blocks with
+//       an AC coefficient outside [-128, 127] go to the exact path),
+//   B = Mq = round(2^F M diag(q)) in three 8-bit limbs (F per quantisation
+//       table, |Mq| < 2^23), DC column zero (the DC term c0 q0 / 8 is exact
+//       and enters through the per-block bias),
+//   D = A B^T per limb, int32 in TMEM: T = acc0 + 2^8 acc1 + 2^16 acc2 + bias
+//       = 2^F (s_tc + 128.5) - e  (mod 2^32; a per-block guard proves no wrap),
+// with the rigorous bound |s_tc - s_ref| <= e 2^-F, e from ||c_AC||_2 and
+// the exact quantisation residual of Mq (Cauchy-Schwarz) plus the float64
+// rounding of the reference.  A sample is proven when floor(T / 2^F) ==
+// floor((T + 2e) / 2^F): then it equals floor(s_ref + 128.5).  Blocks with
+// any unproven sample are recomputed by the exact float64 path as before.
+//
+// CTA: 256 threads, 2 CTAs / SM (TMEM: 256 columns each).  Step s:
+//   staging  - every thread loads its blocks (256-bit loads), writes the
+//              int8 rows into the M=128 operand tiles (K-major, no swizzle)
+//              and the block's bias / bound (int8 DC-free ||c||^2 by DP4A);
+//   units    - Y tiles in two N=32 halves, the chroma tile (Cb and Cr side
+//              by side in TMEM, same rows = same MCU) in four N=16 quarters;
+//              thread 0 issues each unit's 6 / 12 MMAs into one of two TMEM
+//              buffers (mbarrier ping-pong), all 8 warps read their lanes
+//              (warp w: lanes 32(w%4).., half of the unit's columns) and
+//              write the proven u8 samples into the planes of the v3 kernel;
+//   phase B  - exact recompute + the pixel stage of row s-1 (shared with v3).
+namespace tcs {
+constexpr int kThreads = 256;
+constexpr int kCols = 256;                 // TMEM columns per CTA
+constexpr int kBuf0 = 0, kBuf1 = 128;      // two unit buffers (96 columns each)
+constexpr int kFmax = 21;                  // |s| + 128.5 < 2^(31-F) = 1024 at F = 21
+constexpr int kHalfB = 96 * 64;            // B operand of one N=96 half (3 limbs x 32 outputs)
+template <int SUB>
+constexpr int kStrip = SUB == HJ_SUB_444 ? 96 : SUB == HJ_SUB_422 ? 64 : 48;
+template <int SUB>
+struct Dims {
+    static constexpr int S = kStrip<SUB>;
+    static constexpr int NY = SUB == HJ_SUB_444 ? S : SUB == HJ_SUB_422 ? 2 * S : 4 * S;  // Y blocks / step
+    static constexpr int NC = SUB == HJ_SUB_444 ? S : S + 2;                               // chroma MCUs / step
+    static constexpr int YT = (NY + 127) / 128;                                            // Y operand tiles
+    static constexpr int NB = NY + 2 * NC;                                                 // blocks / step
+    static_assert(NC <= 128, "one chroma tile");
+};
+}  // namespace tcs
+
+__device__ const double kMtab[64 * 64] = HJ_MTAB_INIT;
+
+template <int SUB>
+struct SmemTc {
+    using G = GeoT<SUB, tcs::kStrip<SUB>>;
+    using D = tcs::Dims<SUB>;
+    union {
+        struct {
+            alignas(128) uint8_t ay[D::YT][tc::kTileBytes];
+            alignas(128) uint8_t acb[tc::kTileBytes];
+            alignas(128) uint8_t acr[tc::kTileBytes];
+        } a;                                      // MMA A operands (phase A)
+        double g[tcs::kThreads / 8][64];          // exact-path staging (phase B)
+    };
+    alignas(128) uint8_t bm[2][2 * tcs::kHalfB];  // MMA B: [Y, chroma] x two N=96 halves (limb-stacked)
+    alignas(16) uint8_t ys[G::YSLOTS][G::MH * G::YW];
+    alignas(16) uint8_t cbp[SUB == HJ_SUB_444 ? 2 : 1][SUB == HJ_SUB_444 ? 8 * G::YW : 16];
+    alignas(16) uint8_t crp[SUB == HJ_SUB_444 ? 2 : 1][SUB == HJ_SUB_444 ? 8 * G::YW : 16];
+    alignas(16) uint16_t cs[SUB == HJ_SUB_444 ? 1 : G::CROWS][SUB == HJ_SUB_444 ? 8 : G::CW];
+    int qi[3][64];
+    int2 meta[D::NB];                             // per staged block: bias, 2e
+    int flag[D::NB];                              // 1 = queued for the exact path
+    uint32_t queue[2][D::NB];
+    uint32_t qdst[2][D::NB];
+    int n_queue[2];
+    int n_taken[2];
+    alignas(8) uint64_t full[2];
+    alignas(8) uint64_t empty[2];
+    uint32_t tmem;
+    int F[2];
+    float dd[2], gg[2];                           // per table: error and magnitude factors
+    unsigned long long mx[2], dmax[2], gmax[2];   // reductions (positive doubles as bits)
+    int cr_differs;                               // Cr table != Cb table
+};
+
+// Build B (3 limbs of round(2^F M q), canonical K-major) for the luma table
+// (c = 0) and the chroma table (c = 1), and the per-table factors of the
+// screen bound.  128 threads: (c, output i), 64 coefficients each.
+template <int SUB>
+__device__ __forceinline__ void tc_build_b(SmemTc<SUB> &sm, const hj_image_t &im) {
+    const int tid = threadIdx.x;
+    const int c = tid >> 6, i = tid & 63;
+    const int *q = im.q + (c ? 64 : 0);
+    if (tid < 2) sm.mx[tid] = sm.dmax[tid] = sm.gmax[tid] = 0ull;
+    if (tid == 0) sm.cr_differs = 0;
+    __syncthreads();
+    if (tid < 128) {
+        double mx = 0.0;
+        for (int j = 1; j < 64; ++j) mx = fmax(mx, fabs(kMtab[j * 64 + i] * (double)q[j]));
+        atomicMax(&sm.mx[c], (unsigned long long)__double_as_longlong(mx));
+    }
+    __syncthreads();
+    if (tid < 128) {
+        const double mx = __longlong_as_double((long long)sm.mx[c]);
+        int F = tcs::kFmax;
+        if (mx > 0.0) F = min(F, (int)floor(log2(8355711.0 / mx)));  // balanced 3-limb range
+        const double sc = ldexp(1.0, F), isc = ldexp(1.0, -F);
+        double dsum = 0.0, gsum = 0.0;
+        // output i of half h = i >> 5 is row 32 d + (i & 31) of that half's
+        // N = 96 operand, d = limb: one MMA yields all three limb products
+        uint8_t *bh = sm.bm[c] + (i >> 5) * tcs::kHalfB;
+        const int r0 = i & 31;
+        for (int j0 = 0; j0 < 64; j0 += 4) {
+            uint32_t w0 = 0, w1 = 0, w2 = 0;
 #pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        c8[2 * c] = (uint8_t)(c < 4 ? row.x >> (8 * c) : row.y >> (8 * (c - 4)));
+            for (int k = 0; k < 4; ++k) {
+                const int j = j0 + k;
+                const double mq = kMtab[j * 64 + i] * (double)q[j];
+                int v = 0;
+                if (j > 0) {
+                    v = (int)__double2ll_rn(mq * sc);
+                    const double d = (double)v * isc - mq;
+                    dsum = fma(d, d, dsum);
+                    gsum = fma(mq, mq, gsum);
                 }
+                // balanced signed limbs: v = l0 + 2^8 l1 + 2^16 l2, each in [-128, 127]
+                const int l0 = ((v + 128) & 255) - 128;
+                const int v1 = (v - l0) >> 8;
+                const int l1 = ((v1 + 128) & 255) - 128;
+                const int l2 = (v1 - l1) >> 8;
+                w0 |= (uint32_t)(l0 & 255) << (8 * k);
+                w1 |= (uint32_t)(l1 & 255) << (8 * k);
+                w2 |= (uint32_t)(l2 & 255) << (8 * k);
             }
-            if (tid == 0 && n) atomicAdd(&g_exact_blocks, (unsigned long long)n);
+            *reinterpret_cast<uint32_t *>(bh + tc::kmaj(r0, j0)) = w0;
+            *reinterpret_cast<uint32_t *>(bh + tc::kmaj(32 + r0, j0)) = w1;
+            *reinterpret_cast<uint32_t *>(bh + tc::kmaj(64 + r0, j0)) = w2;
+        }
+        atomicMax(&sm.dmax[c], (unsigned long long)__double_as_longlong(sqrt(dsum)));
+        atomicMax(&sm.gmax[c], (unsigned long long)__double_as_longlong(sqrt(gsum)));
+        if (i == 0) sm.F[c] = F;
+        // the chroma B operand is built from the Cb table; a Cr table that
+        // differs (rare: libjpeg and Pillow share table 1) sends Cr blocks
+        // to the exact path
+        if (c == 1 && im.q[64 + i] != im.q[128 + i]) sm.cr_differs = 1;
+    }
+    tc::fence_proxy_async();
+    __syncthreads();
+    if (tid < 2) {
+        // error factor per unit ||c_AC||_2, in value units: the quantisation
+        // residual (rounded up) + the reference's float64 rounding and the
+        // table's own rounding, <= 2^-44 q_max sqrt(63) per unit of ||c||
+        int qmax = 1;
+        for (int j = 0; j < 64; ++j) qmax = max(qmax, im.q[(tid ? 64 : 0) + j]);
+        const double d = __longlong_as_double((long long)sm.dmax[tid]) * (1.0 + 0x1p-20) + 0x1p-41 * qmax;
+        sm.dd[tid] = __double2float_ru(d);
+        sm.gg[tid] = __double2float_ru(__longlong_as_double((long long)sm.gmax[tid]) * (1.0 + 0x1p-20));
+    }
+    __syncthreads();
+}
+
+// Y-block geometry of a step: block b of the step's MCU-row strip ->
+// coefficient index (relative to the row strip start) and plane offset.
+template <int SUB, class G>
+__device__ __forceinline__ int tc_y_off(int b) {
+    if (SUB == HJ_SUB_444) return 8 * b;
+    if (SUB == HJ_SUB_422) return 16 * (b >> 1) + 8 * (b & 1);
+    return ((b & 3) >> 1) * 8 * G::YW + (b >> 2) * 16 + (b & 1) * 8;
+}
+
+// Stage one block: int8 row of the operand tile, bias / bound, range guard.
+// Returns true when the block must take the exact path.
+__device__ __forceinline__ bool tc_stage(const int16_t *__restrict__ src, uint8_t *arow_tile, int row, int q0,
+                                         int F, float dd, float gg, bool direct, int2 &meta) {
+    int4 raw[8];
+    const int4 *s4 = reinterpret_cast<const int4 *>(src);
+#pragma unroll
+    for (int r = 0; r < 8; r += 2) ldg_rows2(s4 + r, raw[r], raw[r + 1]);
+    uint32_t lo[16];
+    uint32_t rng = 0;
+    int n2 = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int4 &v = raw[i >> 1];
+        const uint32_t a = (uint32_t)((i & 1) ? v.z : v.x), b = (uint32_t)((i & 1) ? v.w : v.y);
+        const uint32_t L = __byte_perm(a, b, 0x6420);   // low bytes of 4 coefficients
+        const uint32_t H = __byte_perm(a, b, 0x7531);   // high bytes
+        uint32_t Sg;  // sign of each low byte, replicated (PRMT sign mode; __byte_perm masks it off)
+        asm("prmt.b32 %0, %1, %2, 0xECA8;" : "=r"(Sg) : "r"(a), "r"(b));
+        const uint32_t m = i == 0 ? 0xFFFFFF00u : 0xFFFFFFFFu;  // DC excluded
+        rng |= (H ^ Sg) & m;
+        n2 = __dp4a((int)(L & m), (int)(L & m), n2);
+        lo[i] = L;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        sts128(arow_tile + tc::kmaj(row, 16 * k), make_uint4(lo[4 * k], lo[4 * k + 1], lo[4 * k + 2], lo[4 * k + 3]));
+    const int dc = (int)(short)(raw[0].x & 0xffff);
+    const float dcq = fabsf((float)dc * (float)q0);  // exact: |dc q0| < 2^31 fits 24 bits? bounded below
+    const float nrm = __fsqrt_ru((float)n2);
+    const float scale = __int_as_float((127 + F) << 23);  // 2^F
+    const float eu = __fmul_ru(__fmaf_ru(nrm, dd, __fmul_ru(__fmul_ru(dcq, 1.0000001f), 0x1p-44f)), scale);
+    const int e = (int)ceilf(eu) + 2;
+    // no-wrap guard: |T|, |T + 2e| < 2^31 with |s| <= |dc q0| / 8 + ||c_AC|| G
+    const float sb = __fmaf_ru(nrm, gg, __fmul_ru(__fmul_ru(dcq, 1.0000001f), 0.125f));
+    const bool wrap = __fadd_ru(__fmul_ru(__fadd_ru(sb, 129.0f), scale), 2.0f * (float)e + 8.0f) >= 2.0e9f;
+    const long long bias = ((257ll << F) >> 1) - e + (((long long)dc * q0) << F >> 3);
+    meta = make_int2((int)bias, 2 * e);
+    return direct || rng != 0 || wrap;
+}
+
+template <int SUB>
+__global__ void __launch_bounds__(tcs::kThreads, 2)
+render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ tiles) {
+    using Sm = SmemTc<SUB>;
+    using G = typename Sm::G;
+    using D = tcs::Dims<SUB>;
+    constexpr int NT = tcs::kThreads;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    Sm &sm = *reinterpret_cast<Sm *>(smem_raw);
+
+    const Tile t = tiles[blockIdx.x];
+    const hj_image_t im = images[t.image];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int mpr = im.mcus_per_row;
+    const int S = t.m1 - t.m0;
+    const bool direct = (im.flags & HJ_FLAG_DIRECT_IDCT) != 0;
+    for (int i = tid; i < 192; i += NT) sm.qi[i >> 6][i & 63] = im.q[i];
+    if (tid == 0) {
+        sm.n_queue[0] = sm.n_queue[1] = sm.n_taken[0] = sm.n_taken[1] = 0;
+        tc::mbar_init(&sm.full[0], 1);
+        tc::mbar_init(&sm.full[1], 1);
+        tc::mbar_init(&sm.empty[0], NT / 32);
+        tc::mbar_init(&sm.empty[1], NT / 32);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (warp == 0) tc::tmem_alloc<tcs::kCols>(&sm.tmem);
+    tc_build_b<SUB>(sm, im);  // (contains the barriers that publish the above)
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = sm.tmem;
+    const int F0 = sm.F[0], F1 = sm.F[1];
+    const float dd0 = sm.dd[0], dd1 = sm.dd[1], gg0 = sm.gg[0], gg1 = sm.gg[1];
+    const bool cr_exact = sm.cr_differs != 0;
+
+    const int cm_lo = (SUB == HJ_SUB_444) ? t.m0 : t.m0 - 1;
+    const int n_cm = (SUB == HJ_SUB_444) ? S : S + 2;
+    const int n_yb = (SUB == HJ_SUB_444) ? S : (SUB == HJ_SUB_422 ? 2 * S : 4 * S);
+    constexpr int YB = G::MW / 8 * (G::MH / 8);
+    const int mcu_rows = im.mcu_rows;
+    uint32_t unit = 0;  // running unit counter (TMEM buffer = unit & 1)
+
+    const int s_begin = (SUB == HJ_SUB_420) ? max(t.r0 - 2, -1) : t.r0;
+    const int s_end = t.r1;
+#pragma unroll 1
+    for (int s = s_begin; s <= s_end; ++s) {
+        const int par = s & 1;
+        int *const nq = &sm.n_queue[par];
+        uint32_t *const queue = sm.queue[par];
+        uint32_t *const qdst = sm.qdst[par];
+        const bool do_y = s >= t.r0 && s < t.r1;
+        const int crow = (SUB == HJ_SUB_420) ? s + 1 : s;
+        const bool do_c = (SUB == HJ_SUB_420) ? (crow >= t.r0 - 1 && crow <= t.r1 && crow >= 0 && crow < mcu_rows)
+                                              : do_y;
+        const int64_t yblk0 = ((int64_t)s * mpr + t.m0) * YB;  // first Y block of the step
+        if (tid == 0) {
+            sm.n_queue[par ^ 1] = 0;
+            sm.n_taken[par ^ 1] = 0;
+            const int ny = HJ_PF_L2 ? s + 1 : -1;
+            if (ny >= t.r0 && ny < t.r1) {
+                const int64_t b0 = ((int64_t)ny * mpr + t.m0) * YB;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(im.y + b0 * 64),
+                             "r"((unsigned)(S * YB * 128)));
+            }
+            const int nc = crow + 1;
+            if (HJ_PF_L2 && nc < mcu_rows && nc <= t.r1) {
+                const int c0 = max(cm_lo, 0), c1 = min(cm_lo + n_cm, mpr);
+                const int64_t b0 = (int64_t)nc * mpr + c0;
+                const unsigned bytes = (unsigned)((c1 - c0) * 128);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(im.cb + b0 * 64), "r"(bytes));
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(im.cr + b0 * 64), "r"(bytes));
+            }
         }
 
-        // ---------------- ... overlapped with the pixel stage of MCU row s-1
-        const int R = s - 1;
-        if (!HJ_ABLATE_PIXELS && R >= t.r0 && R < t.r1) {
-            const int y_base = R * G::MH;
-            const int x_base = t.m0 * G::MW;
-            const uint8_t *yp = sm.ys[par ^ 1];
-            int *const taken = &sm.n_taken[par];
-            if constexpr (SUB == HJ_SUB_420) {
-                // item = (MCU column g, row pair p): output rows y_base+2p, +1
-                const int n_items = 8 * S;
-                const int gw = S;
-                const float inv_w = 1.0f / (float)gw;
-                const uint16_t *cnear = &sm.cs[0][0] + (R % 3) * 8 * G::CW;
-                const uint16_t *cnext = &sm.cs[0][0] + ((R + 1) % 3) * 8 * G::CW;
-                // top context of the MCU row's first sample row: the last row
-                // of MCU row R-1 - saved in row 24 when this step's chroma
-                // jobs overwrote its slot, else still in the slot
-                const uint16_t *cprev = do_c ? &sm.cs[24][0] : &sm.cs[0][0] + (((R + 2) % 3) * 8 + 7) * G::CW;
+        // ---------------- staging: int8 operand rows + per-block bounds
+        const int n_y = do_y ? n_yb : 0;
+        const int n_c = do_c ? n_cm : 0;
 #pragma unroll 1
-                for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
-                    const int i = i0;
-                    if (i >= n_items) continue;
-                    // row-major items: adjacent lanes store adjacent 48-byte runs
-                    const int p = __float2int_rd(((float)i + 0.5f) * inv_w), g = i - p * S;
-                    const int y0 = y_base + 2 * p;
-                    if (y0 >= im.height) continue;
-                    const int x0 = x_base + 16 * g;
-                    const int npx = min(16, im.width - x0);
-                    if (npx <= 0) continue;
-                    const int kw = 8 * (g + 1);  // window word of the MCU's chroma column 0
-                    const uint16_t *pn = cnear + p * G::CW + kw;
-                    const uint16_t *pu = p > 0 ? pn - G::CW : (R > 0 ? cprev + kw : pn);
-                    const uint16_t *pd = p < 7 ? pn + G::CW : (R + 1 < mcu_rows ? cnext + kw : pn);
-                    if (kIslow) {
-                        // libjpeg context rows: the real chroma plane ends at row
-                        // ceil(h/2) - 1 (jdmainct.c set_bottom_pointers); box
-                        // replication has no vertical filter
-                        if (lj_box || 8 * R + p >= lj_ch - 1) pd = pn;
-                        if (lj_box) pu = pn;
-                    }
-                    const bool le = left_edge && g == 0, re = right_edge && g == S - 1;
-                    const int c0 = 8 * (t.m0 + g);  // the item's first chroma column
-                    // colsum = 3*near + far per lane (libjpeg h2v2 fancy), 16x scaled
-                    uint32_t n3[10];
-                    load_c10(pn, le, re, n3);
-                    if (kIslow && c0 + 8 >= lj_cw) lj_right_edge(n3, lj_cw, c0);
-#pragma unroll
-                    for (int k = 0; k < 10; ++k) n3[k] = n3[k] * (3u << G::CSH) + 0x00200020u;
-                    const int rows = min(2, im.height - y0);
-#pragma unroll 1
-                    for (int h = 0; h < rows; ++h) {
-                        uint32_t cs10[10];
-                        load_c10(h ? pd : pu, le, re, cs10);
-                        if (kIslow && c0 + 8 >= lj_cw) lj_right_edge(cs10, lj_cw, c0);
-#pragma unroll
-                        for (int k = 0; k < 10; ++k) cs10[k] = (cs10[k] << G::CSH) + n3[k];
-                        // even 16(3cs+prev+8), odd 16(3cs+next+7): each colsum
-                        // carries +2 (x16) from n3, so 3cs+prev already holds
-                        // the +8 and odd subtracts 1 (lanes stay >= 0x80)
-                        uint8_t *dst = im.rgb + ((int64_t)(y0 + h) * im.width + x0) * 3;
-                        const uint4 yv = lds128(yp + (2 * p + h) * G::YW + 16 * g);
-                        if (kIslow && lj_box)
-                            render16_swar<MODE, true>(dst, yv, cs10, 0u, 0u - 0x00100010u, npx);
-                        else
-                            render16_swar<MODE>(dst, yv, cs10, 0u, 0u - 0x00100010u, npx);
-                    }
-                }
-            } else if constexpr (SUB == HJ_SUB_422) {
-                // item = (MCU column g, row y): 16 pixels
-                const int n_items = 8 * S;
-                const int gw = S;
-                const float inv_w = 1.0f / (float)gw;
-                const uint16_t *crow0 = &sm.cs[0][0] + (par ^ 1) * 8 * G::CW;
-#pragma unroll 1
-                for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
-                    const int i = i0;
-                    if (i >= n_items) continue;
-                    const int y = __float2int_rd(((float)i + 0.5f) * inv_w), g = i - y * gw;
-                    const int yy = y_base + y;
-                    if (yy >= im.height) continue;
-                    const int x0 = x_base + 16 * g;
-                    const int npx = min(16, im.width - x0);
-                    if (npx <= 0) continue;
-                    uint32_t c10[10];
-                    load_c10(crow0 + y * G::CW + 8 * (g + 1), left_edge && g == 0, right_edge && g == S - 1, c10);
-                    const int c0 = 8 * (t.m0 + g);
-                    if (kIslow && c0 + 8 >= lj_cw) lj_right_edge(c10, lj_cw, c0);
-#pragma unroll
-                    for (int k = 0; k < 10; ++k) c10[k] = (c10[k] << G::CSH) + 0x00100010u;
-                    // h2v1 on 64x-scaled lanes: even 64(3c+prev+1), odd 64(3c+next+2);
-                    // each sample carries +1/4 (x64), so 3c+prev already holds the +1
-                    uint8_t *dst = im.rgb + ((int64_t)yy * im.width + x0) * 3;
-                    const uint4 yv = lds128(yp + y * G::YW + 16 * g);
-                    if (kIslow && lj_box)
-                        render16_swar<MODE, true>(dst, yv, c10, 0u, 0x00400040u, npx);
-                    else
-                        render16_swar<MODE>(dst, yv, c10, 0u, 0x00400040u, npx);
+        for (int j = tid; j < n_y + 2 * n_c; j += NT) {
+            if (j < n_y) {
+                int2 meta;
+                const bool bad = tc_stage(im.y + (yblk0 + j) * 64, sm.a.ay[j >> 7], j & 127, sm.qi[0][0], F0, dd0,
+                                          gg0, direct, meta);
+                sm.meta[j] = meta;
+                sm.flag[j] = bad;
+                if (bad) {
+                    const uint32_t dst = (uint32_t)(sm.ys[par] + tc_y_off<SUB, G>(j) - smem_raw);
+                    push_exact(nq, queue, qdst, (uint32_t)(yblk0 + j), dst);
                 }
             } else {
-                // item = (MCU pair g, row y): 16 pixels
-                const int gw = (S + 1) / 2;
-                const int n_items = 8 * gw;
-                const float inv_w = 1.0f / (float)gw;
-                const uint8_t *cbp = sm.cbp[par ^ 1], *crp = sm.crp[par ^ 1];
+                const int k = (j - n_y) >= n_c;           // 0: Cb, 1: Cr
+                const int lm = j - n_y - k * n_c;         // chroma window MCU
+                const int m = cm_lo + lm;
+                if (m < 0 || m >= mpr) {
+                    sm.flag[D::NY + k * D::NC + lm] = 1;  // no block: never written, never queued
+                    continue;
+                }
+                const int64_t cblk = (int64_t)crow * mpr + m;
+                int2 meta;
+                const bool bad = tc_stage((k ? im.cr : im.cb) + cblk * 64, k ? sm.a.acr : sm.a.acb, lm, sm.qi[1 + k][0],
+                                          F1, dd1, gg1, direct || (k && cr_exact), meta);
+                sm.meta[D::NY + k * D::NC + lm] = meta;
+                sm.flag[D::NY + k * D::NC + lm] = bad;
+                uint32_t dst;
+                if (SUB == HJ_SUB_444) {
+                    dst = (uint32_t)((k ? sm.crp[par] : sm.cbp[par]) + 8 * lm - smem_raw);
+                } else {
+                    const int cslot = (SUB == HJ_SUB_420) ? (crow % 3) : par;
+                    const int cw0 = cslot * 8 * G::CW + 8 * lm;
+                    dst = ((2u + k) << 30) | (uint32_t)cw0;
+                    if (SUB == HJ_SUB_420 && k == 0) {
+                        // the slot's old row 7 (MCU row crow-3) is the top
+                        // context of MCU row crow-2, drawn this step
+                        uint16_t *save = &sm.cs[24][0] + 8 * lm;
+                        sts128(save, lds128(&sm.cs[0][0] + cw0 + 7 * G::CW));
+                    }
+                }
+                if (bad) push_exact(nq, queue, qdst, ((1u + k) << 30) | (uint32_t)cblk, dst);
+            }
+        }
+        tc::fence_proxy_async();
+        __syncthreads();
+
+        // ---------------- units: MMA (thread 0) -> TMEM -> proven samples
+        const int n_yunits = do_y ? 2 * ((n_yb + 127) >> 7) : 0;
+        const int n_units = n_yunits + (do_c ? 4 : 0);
+        auto issue = [&](int k, uint32_t u) {
+            const uint32_t b = u & 1, dcol = tbase + (b ? tcs::kBuf1 : tcs::kBuf0);
+            if (u >= 2) tc::mbar_wait(&sm.empty[b], ((u - 2) >> 1) & 1);
+            tc::fence_after();
+            constexpr uint32_t id = tc::idesc_i8(96, true, true);
+            // Y unit k: tile k >> 1, half k & 1; chroma unit: (Cb, Cr) x half, order Cb0 Cr0 Cb1 Cr1
+            const int cu = k - n_yunits;
+            const uint32_t a0 = k < n_yunits ? tc::smem_u32(sm.a.ay[k >> 1]) : tc::smem_u32((cu & 1) ? sm.a.acr : sm.a.acb);
+            const uint32_t b0 = tc::smem_u32(sm.bm[k < n_yunits ? 0 : 1]) + (k < n_yunits ? (k & 1) : (cu >> 1)) * tcs::kHalfB;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) tc::mma_i8(dcol, tc::sdesc(a0 + ks * 256), tc::sdesc(b0 + ks * 256), id, ks);
+            tc::commit(&sm.full[b]);
+        };
+        if (tid == 0) {
+            if (n_units > 0) issue(0, unit);
+            if (n_units > 1) issue(1, unit + 1);
+        }
+        const int qd = warp & 3, grp = warp >> 2;
+        const int row = 32 * qd + lane;
+        uint32_t cbk[4] = {0, 0, 0, 0};  // 4:2:x: Cb samples held for the paired Cr unit
 #pragma unroll 1
-                for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
-                    const int i = i0;
-                    if (i >= n_items) continue;
-                    const int y = __float2int_rd(((float)i + 0.5f) * inv_w), g = i - y * gw;
-                    const int yy = y_base + y;
-                    if (yy >= im.height) continue;
-                    const int x0 = x_base + 16 * g;
-                    const int npx = min(min(16, im.width - x0), 8 * (S - 2 * g));
-                    if (npx <= 0) continue;
-                    const int o = y * G::YW + 16 * g;
-                    render16_444<MODE>(im.rgb + ((int64_t)yy * im.width + x0) * 3, lds128(yp + o), lds128(cbp + o),
-                                 lds128(crp + o), npx);
+        for (int k = 0; k < n_units; ++k, ++unit) {
+            const uint32_t b = unit & 1;
+            const uint32_t tl = tbase + ((uint32_t)(32 * qd) << 16) + (b ? tcs::kBuf1 : tcs::kBuf0);
+            tc::mbar_wait(&sm.full[b], (unit >> 1) & 1);
+            tc::fence_after();
+            __syncwarp();  // the tcgen05.ld below are warp-collective (.sync.aligned)
+            uint32_t a0[16], a1[16], a2[16];  // limbs 0..2 of this thread's 16 outputs
+            tc::ld16(tl + 16 * grp, a0);
+            tc::ld16(tl + 32 + 16 * grp, a1);
+            tc::ld16(tl + 64 + 16 * grp, a2);
+            tc::wait_ld();
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sm.empty[b]);
+            if (tid == 0 && k + 2 < n_units) issue(k + 2, unit + 2);
+            // this thread's block (TMEM lane) and its two sample rows 4h + 2 grp (+1)
+            const bool is_y = k < n_yunits;
+            const int cu = k - n_yunits, cc = cu & 1;
+            const int h = is_y ? (k & 1) : (cu >> 1);
+            const int yb = (k >> 1) * 128 + row, lm = row;
+            const int fi = is_y ? yb : D::NY + cc * D::NC + lm;
+            const bool valid = is_y ? yb < n_yb : (lm < n_cm && cm_lo + lm >= 0 && cm_lo + lm < mpr);
+            if (valid) {
+                const int Fk = is_y ? F0 : F1;
+                const int flagged = sm.flag[fi];
+                const int2 mt = sm.meta[fi];
+                uint32_t fail = 0;
+                int n[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const uint32_t T = a0[i] + (uint32_t)mt.x + (a1[i] << 8) + (a2[i] << 16);
+                    fail |= T ^ (T + (uint32_t)mt.y);
+                    n[i] = (int)T >> Fk;
+                }
+                const uint32_t w0 = pack4(n[0], n[1], n[2], n[3]), w1 = pack4(n[4], n[5], n[6], n[7]);
+                const uint32_t w2 = pack4(n[8], n[9], n[10], n[11]), w3 = pack4(n[12], n[13], n[14], n[15]);
+                const int srow = 4 * h + 2 * grp;
+                const int cslot = (SUB == HJ_SUB_420) ? (crow % 3) : par;
+                if (is_y) {
+                    uint8_t *dst = sm.ys[par] + tc_y_off<SUB, G>(yb) + srow * G::YW;
+                    *reinterpret_cast<uint2 *>(dst) = make_uint2(w0, w1);
+                    *reinterpret_cast<uint2 *>(dst + G::YW) = make_uint2(w2, w3);
+                } else if (SUB == HJ_SUB_444) {
+                    uint8_t *dst = (cc ? sm.crp[par] : sm.cbp[par]) + 8 * lm + srow * G::YW;
+                    *reinterpret_cast<uint2 *>(dst) = make_uint2(w0, w1);
+                    *reinterpret_cast<uint2 *>(dst + G::YW) = make_uint2(w2, w3);
+                } else if (cc == 0) {
+                    cbk[0] = w0, cbk[1] = w1, cbk[2] = w2, cbk[3] = w3;  // paired with the Cr unit next
+                } else {
+                    uint16_t *cdst = &sm.cs[0][0] + cslot * 8 * G::CW + 8 * lm + srow * G::CW;
+                    sts128(cdst, make_uint4(__byte_perm(cbk[0], w0, 0x5140), __byte_perm(cbk[0], w0, 0x7362),
+                                            __byte_perm(cbk[1], w1, 0x5140), __byte_perm(cbk[1], w1, 0x7362)));
+                    sts128(cdst + G::CW, make_uint4(__byte_perm(cbk[2], w2, 0x5140), __byte_perm(cbk[2], w2, 0x7362),
+                                                    __byte_perm(cbk[3], w3, 0x5140), __byte_perm(cbk[3], w3, 0x7362)));
+                }
+                if (!flagged && (fail >> Fk) != 0 && atomicExch(&sm.flag[fi], 1) == 0) {
+                    if (is_y) {
+                        push_exact(nq, queue, qdst, (uint32_t)(yblk0 + yb),
+                                   (uint32_t)(sm.ys[par] + tc_y_off<SUB, G>(yb) - smem_raw));
+                        if (HJ_PF_EXACT) prefetch_l1(im.y + (yblk0 + yb) * 64);
+                    } else {
+                        const int64_t cblk = (int64_t)crow * mpr + cm_lo + lm;
+                        const uint32_t dst = SUB == HJ_SUB_444
+                                                 ? (uint32_t)((cc ? sm.crp[par] : sm.cbp[par]) + 8 * lm - smem_raw)
+                                                 : ((2u + cc) << 30) | (uint32_t)(cslot * 8 * G::CW + 8 * lm);
+                        push_exact(nq, queue, qdst, ((1u + cc) << 30) | (uint32_t)cblk, dst);
+                        if (HJ_PF_EXACT) prefetch_l1((cc ? im.cr : im.cb) + cblk * 64);
+                    }
                 }
             }
         }
         __syncthreads();
+
+        // ---------------- phase B: exact recompute ∥ pixel stage of row s-1
+        exact_phase<SUB, kModeRef, G, NT>(sm, smem_raw, im, par, direct);
+        pixel_phase<SUB, kModeRef, G>(sm, im, t, s, par, do_c);
+        __syncthreads();
     }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<tcs::kCols>(tbase);
+}
+
+// two CTAs per SM: (228 KB - 2 x 1 KB reserved) / 2
+static_assert(sizeof(SmemTc<HJ_SUB_444>) <= 113 * 1024, "4:4:4 tensor-core smem");
+static_assert(sizeof(SmemTc<HJ_SUB_422>) <= 113 * 1024, "4:2:2 tensor-core smem");
+static_assert(sizeof(SmemTc<HJ_SUB_420>) <= 113 * 1024, "4:2:0 tensor-core smem");
+
+std::atomic<unsigned long long> g_tc_launches{0};
+
+template <int SUB>
+cudaError_t launch_tc(const hj_image_t *images, const Tile *tiles, int n_tiles, cudaStream_t stream) {
+    g_tc_launches.fetch_add(1, std::memory_order_relaxed);
+    static std::atomic<uint64_t> configured{0};
+    const int bytes = (int)sizeof(SmemTc<SUB>);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(configured.load(std::memory_order_acquire) & bit)) {
+        e = cudaFuncSetAttribute(render_tc_kernel<SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e != cudaSuccess) return e;
+        configured.fetch_or(bit, std::memory_order_release);
+    }
+    render_tc_kernel<SUB><<<n_tiles, tcs::kThreads, bytes, stream>>>(images, tiles);
+    return cudaGetLastError();
 }
 
 template <int SUB, int MODE>
@@ -1230,10 +1726,17 @@ cudaError_t launch_sub(const hj_image_t *images, const Tile *tiles, int n_tiles,
 
 }  // namespace
 
+unsigned long long tc_launch_count() { return g_tc_launches.load(); }
+
 unsigned long long exact_block_count() {
     unsigned long long v = 0;
     cudaMemcpyFromSymbol(&v, g_exact_blocks, sizeof(v));
     return v;
+}
+
+size_t render_smem_bytes_tc(int sub) {
+    return sub == HJ_SUB_444 ? sizeof(SmemTc<HJ_SUB_444>)
+         : sub == HJ_SUB_422 ? sizeof(SmemTc<HJ_SUB_422>) : sizeof(SmemTc<HJ_SUB_420>);
 }
 
 size_t render_smem_bytes(int sub) {
@@ -1246,6 +1749,11 @@ size_t render_smem_bytes(int sub) {
 cudaError_t launch_render(int sub, int mode, const hj_image_t *images, const Tile *tiles, int n_tiles,
                           cudaStream_t stream) {
     if (n_tiles <= 0) return cudaSuccess;
+    if (mode == kModeRefTc) {
+        if (sub == HJ_SUB_444) return launch_tc<HJ_SUB_444>(images, tiles, n_tiles, stream);
+        if (sub == HJ_SUB_422) return launch_tc<HJ_SUB_422>(images, tiles, n_tiles, stream);
+        return launch_tc<HJ_SUB_420>(images, tiles, n_tiles, stream);
+    }
     if (mode == kModeIslow) {
         if (sub == HJ_SUB_444) return launch_sub<HJ_SUB_444, kModeIslow>(images, tiles, n_tiles, stream);
         if (sub == HJ_SUB_422) return launch_sub<HJ_SUB_422, kModeIslow>(images, tiles, n_tiles, stream);

@@ -68,7 +68,22 @@ inline int strip_width(int sub) {
 
 // Decode modes of the render kernel: the reference's float64 arithmetic
 // (AAN "fast" or "direct" per image flag) or libjpeg's integer "islow".
-enum { kModeRef = 0, kModeIslow = 1 };
+// kModeRefTc: the reference's arithmetic with the IDCT screen on the tensor
+// cores (render_tc_kernel, v4); kModeRef keeps the FP32-screen kernel (v3),
+// used for "direct" images and chroma tables that differ between Cb and Cr.
+enum { kModeRef = 0, kModeIslow = 1, kModeRefTc = 2 };
+
+// Tensor-core kernel geometry: 256-thread CTAs, 2 per SM (TMEM), strips of
+// 96 / 64 / 48 MCUs for 4:4:4 / 4:2:2 / 4:2:0.
+constexpr int kTcThreads = 256;
+constexpr int kTcCtasPerSm = 2;
+constexpr int tc_strip(int sub) { return sub == HJ_SUB_444 ? 96 : sub == HJ_SUB_422 ? 64 : 48; }
+
+// Plan group kinds (hj_api.cu): the IDCT path an image takes.
+enum { kKindTc = 0, kKindDirect = 1, kKindIslow = 2, kKindSimt = 3 };
+inline int mode_of_kind(int kind) {
+    return kind == kKindTc ? kModeRefTc : kind == kKindIslow ? kModeIslow : kModeRef;
+}
 
 // Launch the render kernel for `n_tiles` tiles of one subsampling family.
 // `images` and `tiles` are device arrays.
@@ -77,6 +92,8 @@ cudaError_t launch_render(int subsampling, int mode, const hj_image_t *images,
 
 // Blocks the FP32 screen sent to the exact float64 path, all launches so far.
 unsigned long long exact_block_count();
+// Tensor-core screen kernel launches so far.
+unsigned long long tc_launch_count();
 
 // Single-block transforms (reference per-block API).
 cudaError_t launch_idct_blocks(const int32_t *deq, int64_t n, uint8_t *out, double *out_f64,
