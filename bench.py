@@ -66,7 +66,8 @@ def parse_args():
     ap.add_argument("--batch", type=int, default=0, help="images per GPU per step (0 = default)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = auto")
     ap.add_argument("--e2e-chunk", type=int, default=4, help="images per pipelined H2D/render/D2H chunk")
-    ap.add_argument("--e2e-threads", type=int, default=4, help="host threads calling the render_rows plugin")
+    ap.add_argument("--e2e-threads", type=int, default=8,
+                    help="host threads calling the render_rows plugin (the reference's lanes call it from a pool)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-variants", action="store_true",
                     help="4:4:4/4:2:2: time the shipped/patched/fallback reference builds, 1 and N processes")
@@ -862,14 +863,19 @@ def main():
         fn(c.y_blocks, c.cb_blocks, c.cr_blocks, qts[i], out_arrays[i], w, h, mpr, row0, n_rows, idct_arg(args))
 
     n_thr = args.e2e_threads
+    from paper_1311_5304_b200 import _lib as hjlib
     with ThreadPoolExecutor(n_thr) as ex:
         for _ in range(2):
             list(ex.map(one, range(batch)))
         barrier(pg)
+        h2d0 = hjlib.lib.hj_h2d_bytes()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             list(ex.map(one, range(batch)))
         e2e_s = allreduce_max(pg, time.perf_counter() - t0)
+        # bytes the plugin really moved host->device (packed coefficients when
+        # the packed transfer is on), per step
+        plugin_h2d = (hjlib.lib.hj_h2d_bytes() - h2d0) // e2e_steps
     e2e_value = px_all * e2e_steps / e2e_s / 1e6
     e2e_lane_value = px_all * e2e_steps / e2e_lane_s / 1e6
     # the e2e output must be the kernel's output: spot-check one image against the oracle
@@ -918,10 +924,14 @@ def main():
                          "traffic": ncu_traffic(profile_key(args)) if args.batch == 0 else None,
                          "kernel_ms": round(kernel_ms, 5)},
             "e2e": {"value": round(e2e_value, 1), "unit": "Mpix/s",
-                    "h2d_bytes_per_step": io["h2d_bytes"], "d2h_bytes_per_step": io["d2h_bytes"],
+                    "h2d_bytes_per_step": int(plugin_h2d), "d2h_bytes_per_step": io["d2h_bytes"],
+                    "dense_h2d_bytes_per_step": io["h2d_bytes"],
+                    "packed_h2d": bool(hjlib.lib.hj_packed_h2d_active()),
                     "steps": e2e_steps, "bit_exact_vs_oracle": exact,
                     "api": f"kernels.cuda.render_rows_{sub} (reference backend contract) per image from "
-                           f"{n_thr} host threads, pinned host buffers",
+                           f"{n_thr} host threads, pinned host buffers"
+                           + (", coefficients packed on the host (nonzero masks + int8/int16 values) "
+                              "and expanded on the GPU" if hjlib.lib.hj_packed_h2d_active() else ""),
                     "pipelined_lane_mpix_s": round(e2e_lane_value, 1)},
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),

@@ -18,7 +18,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhetjpeg_b200.so")
-SOURCES = ["hj_render.cu", "hj_blockops.cu", "hj_api.cu", "hj_huffman.cpp", "hj_sched.cpp"]
+SOURCES = ["hj_render.cu", "hj_blockops.cu", "hj_api.cu", "hj_huffman.cpp", "hj_sched.cpp", "hj_pack.cpp"]
 HEADERS = ["hj_render.cuh", "hj_common.cuh", "hj_screen.h", "hj_tables.h", "hj_huffman.h", "hj_error.h",
            os.path.join("..", "..", "include", "hetjpeg_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include "hj_error.h"
+#include "hj_pack.h"
 #include "hj_render.cuh"
 
 // tile-planner model parameters (choose_rows_per_tile)
@@ -313,12 +314,18 @@ struct SyncCtx {
     void *misc = nullptr;  // q (768 B) + image desc + tiles
     size_t misc_bytes = 0;
     std::vector<uint8_t> host_plan;  // staging of [image desc][tiles]
+    void *hpack = nullptr;           // page-locked packed coefficients (hj_pack.h)
+    size_t hpack_bytes = 0;
+    void *dpack = nullptr;           // their device copy
+    size_t dpack_bytes = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     void release() {
         if (device >= 0) {
             cudaFree(coef);
             cudaFree(rgb);
             cudaFree(misc);
+            cudaFree(dpack);
+            if (hpack) cudaFreeHost(hpack);
             for (auto &e : ev)
                 if (e) cudaEventDestroy(e);
             if (stream) cudaStreamDestroy(stream);
@@ -339,6 +346,43 @@ hj_status ensure(void **p, size_t *have, size_t need) {
     return HJ_OK;
 }
 
+hj_status ensure_host(void **p, size_t *have, size_t need) {
+    if (*have >= need) return HJ_OK;
+    size_t n = std::max(need, *have * 2);
+    if (*p) cudaFreeHost(*p);
+    *p = nullptr;
+    *have = 0;
+    HJ_CUDA(cudaHostAlloc(p, n, cudaHostAllocDefault));
+    *have = n;
+    return HJ_OK;
+}
+
+// Packed coefficient transfer of the synchronous drop-in (hj_pack.h): on by
+// default where the host has AVX-512 (VBMI2); HJ_PACK_H2D=0 / =1 forces it.
+std::atomic<int> g_pack_mode{-1};  // -1: default, 0 off, 1 on (hj_set_packed_h2d)
+// Packing costs host time (~10 GB/s per core with AVX-512) to save PCIe
+// time (~50 GB/s per direction, shared): it pays when several host threads
+// drive the drop-in at once and the link is the bottleneck, not for a lone
+// caller.  Default: pack when >= kPackMinCallers calls are in flight.
+constexpr int kPackMinCallers = 4;
+constexpr int64_t kPackProbe = 4096;     // blocks packed before the size check
+constexpr double kPackMaxRatio = 0.45;   // pack only below this fraction of the dense bytes
+std::atomic<int> g_inflight{0};
+int pack_env() {
+    static const int env = [] {
+        const char *v = std::getenv("HJ_PACK_H2D");
+        return v && v[0] ? (v[0] != '0' ? 1 : 0) : -1;
+    }();
+    return env;
+}
+bool pack_h2d_on(int inflight) {
+    const int m = g_pack_mode.load(std::memory_order_relaxed);
+    if (m >= 0) return m != 0;
+    if (pack_env() >= 0) return pack_env() != 0;
+    return hj::pack_has_avx512() && inflight >= kPackMinCallers;
+}
+std::atomic<uint64_t> g_h2d_bytes{0};
+
 hj_status ctx_get(SyncCtx **out) {
     int dev = 0;
     HJ_CUDA(cudaGetDevice(&dev));
@@ -347,8 +391,8 @@ hj_status ctx_get(SyncCtx **out) {
         if (c.device >= 0) {
             c.release();
             c.device = -1;
-            c.coef = c.rgb = c.misc = nullptr;
-            c.coef_bytes = c.rgb_bytes = c.misc_bytes = 0;
+            c.coef = c.rgb = c.misc = c.dpack = c.hpack = nullptr;
+            c.coef_bytes = c.rgb_bytes = c.misc_bytes = c.dpack_bytes = c.hpack_bytes = 0;
             for (auto &e : c.ev) e = nullptr;
             c.stream = nullptr;
         }
@@ -618,6 +662,33 @@ hj_status hj_pipeline_huffman(const hj_pipe_image_t *images, int32_t n_images, i
 
 uint64_t hj_exact_block_count(void) { return hj::exact_block_count(); }
 uint64_t hj_tc_launch_count(void) { return hj::tc_launch_count(); }
+uint64_t hj_h2d_bytes(void) { return g_h2d_bytes.load(); }
+hj_status hj_set_packed_h2d(int32_t mode) {
+    if (mode < -1 || mode > 1) return fail(HJ_ERR_ARG, "packed_h2d mode must be -1, 0 or 1");
+    g_pack_mode.store(mode);
+    return HJ_OK;
+}
+int32_t hj_packed_h2d_active(void) {
+    const int m = g_pack_mode.load(std::memory_order_relaxed);
+    if (m >= 0) return m;
+    if (pack_env() >= 0) return pack_env();
+    return hj::pack_has_avx512() ? 2 : 0;  // 2: automatic (when >= kPackMinCallers calls are in flight)
+}
+
+int64_t hj_pack_blocks(const int16_t *src, int64_t n, uint64_t *mask, uint32_t *off, int16_t *dc, uint8_t *vals) {
+    if (n < 0 || (n > 0 && (!src || !mask || !off || !dc || !vals))) {
+        fail(HJ_ERR_ARG, "hj_pack_blocks: bad arguments");
+        return -1;
+    }
+    return (int64_t)hj::pack_blocks(src, n, mask, off, dc, vals, 0);
+}
+hj_status hj_unpack_blocks_host(const uint64_t *mask, const uint32_t *off, const int16_t *dc, const uint8_t *vals,
+                                int64_t n, int16_t *dst) {
+    if (n < 0 || (n > 0 && (!mask || !off || !dc || !vals || !dst)))
+        return fail(HJ_ERR_ARG, "hj_unpack_blocks_host: bad arguments");
+    hj::unpack_blocks_host(mask, off, dc, vals, n, dst);
+    return HJ_OK;
+}
 
 static hj_status render_rows_impl(const int16_t *y, const int16_t *cb, const int16_t *cr,
                                   const int32_t *q3x64, uint8_t *rgb, int32_t width, int32_t height,
@@ -686,11 +757,78 @@ static hj_status render_rows_impl(const int16_t *y, const int16_t *cb, const int
     std::memcpy(c->host_plan.data() + img_off, &im, sizeof(im));
     if (!tiles.empty()) std::memcpy(c->host_plan.data() + tile_off, tiles.data(), sizeof(hj::Tile) * tiles.size());
 
+    const int16_t *hy = y + (int64_t)row0 * per_row_y * 64;
+    const int16_t *hcb = cb + (int64_t)c_lo * per_row_c * 64, *hcr = cr + (int64_t)c_lo * per_row_c * 64;
+    const int64_t nblk = nyb + 2 * ncb;
+    // packed transfer (hj_pack.h): one record [masks | offsets | DC | values]
+    // for the call's blocks, one copy, one unpack launch.  The first
+    // kPackProbe blocks are packed first: a block mix that does not shrink to
+    // under kPackMaxRatio of the dense bytes (high-quality, busy images) is
+    // sent dense - packing costs host time it would not win back.
+    const int inflight = g_inflight.fetch_add(1, std::memory_order_relaxed) + 1;
+    struct Leave {
+        ~Leave() { g_inflight.fetch_sub(1, std::memory_order_relaxed); }
+    } leave;
+    bool pack = pack_h2d_on(inflight) && nblk > 0 && hj::pack_vals_bound(nblk) < 0x7fffffffull;
+    const size_t rec_hdr = ((size_t)nblk * 14 + 15) & ~(size_t)15;
+    const size_t tab_off = (misc_need + 15) & ~(size_t)15;  // record offset table, after the plan
+    size_t rec_bytes = 0;
+    const bool forced = g_pack_mode.load(std::memory_order_relaxed) == 1 || pack_env() == 1;
+    if (pack && !forced) {
+        // probe: pack the first Y blocks into scratch and keep packing only
+        // if they shrink enough (nothing large is allocated for a call that
+        // ends up dense)
+        thread_local std::vector<uint8_t> scratch;
+        const int64_t np = std::min<int64_t>(kPackProbe, nyb > 0 ? nyb : nblk);
+        const int16_t *ps = nyb > 0 ? hy : hcb;
+        scratch.resize((size_t)np * 14 + hj::pack_vals_bound(np));
+        uint8_t *sp = scratch.data();
+        const size_t vb = hj::pack_blocks(ps, np, reinterpret_cast<uint64_t *>(sp),
+                                          reinterpret_cast<uint32_t *>(sp + np * 8),
+                                          reinterpret_cast<int16_t *>(sp + np * 12), sp + np * 14, 0);
+        if ((double)(14 * np + vb) > kPackMaxRatio * 128.0 * (double)np) pack = false;
+    }
+    if (pack) {
+        st = ensure_host(&c->hpack, &c->hpack_bytes, rec_hdr + hj::pack_vals_bound(nblk));
+        if (st != HJ_OK) return st;
+        uint8_t *hp = static_cast<uint8_t *>(c->hpack);
+        uint64_t *hm = reinterpret_cast<uint64_t *>(hp);
+        uint32_t *ho = reinterpret_cast<uint32_t *>(hp + (size_t)nblk * 8);
+        int16_t *hd = reinterpret_cast<int16_t *>(hp + (size_t)nblk * 12);
+        uint8_t *hv = hp + rec_hdr;
+        size_t vb = hj::pack_blocks(hy, nyb, hm, ho, hd, hv, 0);
+        vb += hj::pack_blocks(hcb, ncb, hm + nyb, ho + nyb, hd + nyb, hv + vb, vb);
+        vb += hj::pack_blocks(hcr, ncb, hm + nyb + ncb, ho + nyb + ncb, hd + nyb + ncb, hv + vb, vb);
+        rec_bytes = rec_hdr + vb;
+        st = ensure(&c->dpack, &c->dpack_bytes, rec_bytes);
+        if (st == HJ_OK) st = ensure(&c->misc, &c->misc_bytes, tab_off + 8);
+        if (st != HJ_OK) return st;
+        misc = static_cast<uint8_t *>(c->misc);
+        im.q = reinterpret_cast<const int32_t *>(misc);
+        std::memcpy(c->host_plan.data() + img_off, &im, sizeof(im));
+        c->host_plan.resize(tab_off + 8);
+        std::memset(c->host_plan.data() + tab_off, 0, 8);  // one record at offset 0
+    }
     if (phase_ms) HJ_CUDA(cudaEventRecord(c->ev[0], c->stream));
-    HJ_CUDA(cudaMemcpyAsync(dy, y + (int64_t)row0 * per_row_y * 64, nyb * 128, cudaMemcpyHostToDevice, c->stream));
-    HJ_CUDA(cudaMemcpyAsync(dcb, cb + (int64_t)c_lo * per_row_c * 64, ncb * 128, cudaMemcpyHostToDevice, c->stream));
-    HJ_CUDA(cudaMemcpyAsync(dcr, cr + (int64_t)c_lo * per_row_c * 64, ncb * 128, cudaMemcpyHostToDevice, c->stream));
-    HJ_CUDA(cudaMemcpyAsync(misc, c->host_plan.data(), misc_need, cudaMemcpyHostToDevice, c->stream));
+    if (pack) {
+        HJ_CUDA(cudaMemcpyAsync(c->dpack, c->hpack, rec_bytes, cudaMemcpyHostToDevice, c->stream));
+        g_h2d_bytes.fetch_add(rec_bytes, std::memory_order_relaxed);
+    } else {
+        HJ_CUDA(cudaMemcpyAsync(dy, hy, nyb * 128, cudaMemcpyHostToDevice, c->stream));
+        HJ_CUDA(cudaMemcpyAsync(dcb, hcb, ncb * 128, cudaMemcpyHostToDevice, c->stream));
+        HJ_CUDA(cudaMemcpyAsync(dcr, hcr, ncb * 128, cudaMemcpyHostToDevice, c->stream));
+        g_h2d_bytes.fetch_add((size_t)nblk * 128, std::memory_order_relaxed);
+    }
+    const size_t plan_bytes = c->host_plan.size();
+    HJ_CUDA(cudaMemcpyAsync(misc, c->host_plan.data(), plan_bytes, cudaMemcpyHostToDevice, c->stream));
+    g_h2d_bytes.fetch_add(plan_bytes, std::memory_order_relaxed);
+    if (pack) {
+        cudaError_t e = hj::launch_unpack_blocks(static_cast<const uint8_t *>(c->dpack),
+                                                 reinterpret_cast<const uint64_t *>(misc + tab_off), nblk, rec_hdr,
+                                                 nblk, dy, c->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "unpack kernel launch");
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
     if (phase_ms) HJ_CUDA(cudaEventRecord(c->ev[1], c->stream));
     const hj_image_t *dimg = reinterpret_cast<const hj_image_t *>(misc + img_off);
     const hj::Tile *dtiles = reinterpret_cast<const hj::Tile *>(misc + tile_off);

@@ -82,6 +82,48 @@ __global__ void upsample_422_kernel(const uint8_t *__restrict__ rows, const int1
     o[15] = r < 0 ? s[7] : (3 * s[7] + r + 2) >> 2;
 }
 
+// Packed coefficient transfer (hj_pack.h): expand one block per thread back
+// into the dense int16 CoefficientBuffer layout (lossless).
+template <bool WIDE>
+__device__ __forceinline__ void unpack_one(uint64_t m, int dc, const uint8_t *__restrict__ v, uint32_t (&w)[32]) {
+    int idx = 0;
+#pragma unroll
+    for (int k = 0; k < 64; k += 2) {
+        int a = 0, c = 0;
+        if (k == 0) {
+            a = dc;
+        } else if ((m >> k) & 1) {
+            a = WIDE ? (int)*reinterpret_cast<const int16_t *>(v + 2 * idx) : (int)(int8_t)v[idx];
+            ++idx;
+        }
+        if ((m >> (k + 1)) & 1) {
+            c = WIDE ? (int)*reinterpret_cast<const int16_t *>(v + 2 * idx) : (int)(int8_t)v[idx];
+            ++idx;
+        }
+        w[k >> 1] = (uint32_t)(uint16_t)a | ((uint32_t)(uint16_t)c << 16);
+    }
+}
+
+// Records of `chunk` blocks at byte offsets tab[k] of `pack`: masks (8 B per
+// block slot) | offsets (4) | DC (2) | values at rec_hdr.
+__global__ void unpack_blocks_kernel(const uint8_t *__restrict__ pack, const uint64_t *__restrict__ tab,
+                                     int64_t chunk, size_t rec_hdr, int64_t n, int16_t *__restrict__ out) {
+    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= n) return;
+    const int64_t k = b / chunk, i = b - k * chunk;
+    const uint8_t *rec = pack + tab[k];
+    const uint64_t m = reinterpret_cast<const uint64_t *>(rec)[i];
+    const uint32_t o = reinterpret_cast<const uint32_t *>(rec + chunk * 8)[i];
+    const int dc = reinterpret_cast<const int16_t *>(rec + chunk * 12)[i];
+    const uint8_t *v = rec + rec_hdr + (o & 0x7fffffffu);
+    uint32_t w[32];
+    if (o >> 31) unpack_one<true>(m, dc, v, w);
+    else unpack_one<false>(m, dc, v, w);
+    uint4 *d = reinterpret_cast<uint4 *>(out + b * 64);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+}
+
 }  // namespace
 
 cudaError_t launch_upsample_422(const uint8_t *rows, const int16_t *left, const int16_t *right, int32_t *out,
@@ -107,4 +149,14 @@ cudaError_t launch_ycbcr(const uint8_t *y, const uint8_t *cb, const uint8_t *cr,
     return cudaGetLastError();
 }
 
+}  // namespace hj
+
+namespace hj {
+cudaError_t launch_unpack_blocks(const uint8_t *pack, const uint64_t *tab, int64_t chunk, size_t rec_hdr, int64_t n,
+                                 int16_t *out, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    const int t = 256;
+    unpack_blocks_kernel<<<(unsigned)((n + t - 1) / t), t, 0, stream>>>(pack, tab, chunk, rec_hdr, n, out);
+    return cudaGetLastError();
+}
 }  // namespace hj

@@ -100,6 +100,10 @@ cudaError_t launch_idct_blocks(const int32_t *deq, int64_t n, uint8_t *out, doub
                                bool direct, cudaStream_t stream);
 cudaError_t launch_upsample_422(const uint8_t *rows, const int16_t *left, const int16_t *right,
                                int32_t *out, int64_t n, cudaStream_t stream);
+// Packed coefficient transfer (hj_pack.h): dense int16 blocks from records of
+// `chunk` blocks (masks | offsets | DC | values at rec_hdr) at offsets tab[k].
+cudaError_t launch_unpack_blocks(const uint8_t *pack, const uint64_t *tab, int64_t chunk, size_t rec_hdr, int64_t n,
+                                 int16_t *out, cudaStream_t stream);
 cudaError_t launch_ycbcr(const uint8_t *y, const uint8_t *cb, const uint8_t *cr, uint8_t *rgb,
                          int64_t n, cudaStream_t stream);
 
