@@ -367,6 +367,10 @@ std::atomic<int> g_pack_mode{-1};  // -1: default, 0 off, 1 on (hj_set_packed_h2
 constexpr int kPackMinCallers = 4;
 constexpr int64_t kPackProbe = 4096;     // blocks packed before the size check
 constexpr double kPackMaxRatio = 0.45;   // pack only below this fraction of the dense bytes
+// Large calls stay dense: one thread packs ~10 GB/s while the call's dense
+// copy alone runs at ~50 GB/s, and a multi-MB pinned staging buffer per
+// calling thread is not worth it (measured: 24 MP 4:2:0 images 13.4k -> 2.0k)
+constexpr int64_t kPackMaxBlocks = 1 << 16;  // 8 MB of dense coefficients
 std::atomic<int> g_inflight{0};
 int pack_env() {
     static const int env = [] {
@@ -769,11 +773,12 @@ static hj_status render_rows_impl(const int16_t *y, const int16_t *cb, const int
     struct Leave {
         ~Leave() { g_inflight.fetch_sub(1, std::memory_order_relaxed); }
     } leave;
-    bool pack = pack_h2d_on(inflight) && nblk > 0 && hj::pack_vals_bound(nblk) < 0x7fffffffull;
+    const bool forced = g_pack_mode.load(std::memory_order_relaxed) == 1 || pack_env() == 1;
+    bool pack = pack_h2d_on(inflight) && nblk > 0 && hj::pack_vals_bound(nblk) < 0x7fffffffull &&
+                (forced || nblk <= kPackMaxBlocks);
     const size_t rec_hdr = ((size_t)nblk * 14 + 15) & ~(size_t)15;
     const size_t tab_off = (misc_need + 15) & ~(size_t)15;  // record offset table, after the plan
     size_t rec_bytes = 0;
-    const bool forced = g_pack_mode.load(std::memory_order_relaxed) == 1 || pack_env() == 1;
     if (pack && !forced) {
         // probe: pack the first Y blocks into scratch and keep packing only
         // if they shrink enough (nothing large is allocated for a call that
