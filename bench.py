@@ -76,7 +76,9 @@ def parse_args():
                          "renders its MCU-row range of the SAME images (strong scaling, "
                          "BASELINE config 4; 4:2:0 ranks also load one chroma MCU row of context)")
     ap.add_argument("--no-amdahl", action="store_true", help="skip the Huffman-inclusive pipeline run")
-    ap.add_argument("--amdahl-images", type=int, default=32, help="images per rank in the pipeline run")
+    ap.add_argument("--amdahl-images", type=int, default=0,
+                    help="images per rank in the pipeline run (0 = auto: >= 32 and >= 64 Mpx per rank, so "
+                         "pipeline fill / drain does not dominate small-image batches)")
     ap.add_argument("--idct", default="fast", choices=["fast", "direct", "islow"],
                     help="fast/direct = the reference's float64 AAN / direct basis (bit-exact vs the reference); "
                          "islow = libjpeg's integer decode (north_star's jidctint mode, exact vs libjpeg-turbo)")
@@ -306,6 +308,13 @@ def port_rate(images, wl, threads, budget_s=2.0):
         oracle.render(c.y_blocks, c.cb_blocks, c.cr_blocks, q, w, h, sub, True, threads)
         n += 1
     return round(n * w * h / (time.perf_counter() - t0) / 1e6, 2)
+
+
+def amdahl_n(args, wl):
+    """Images per rank of the Huffman-inclusive pipeline run."""
+    if args.amdahl_images:
+        return args.amdahl_images
+    return max(32, -(-64_000_000 // (wl[0] * wl[1])))
 
 
 def amdahl_run(images, wl, world, pg, n_images, reserve=0, idct="fast"):
@@ -887,15 +896,15 @@ def main():
     # ---- end to end INCLUDING host Huffman: the paper's Amdahl metric
     amdahl = None
     if not args.no_amdahl and rows_mode:
-        amdahl = amdahl_rows(images, wl, world, pg, args.amdahl_images, row0, n_rows, args.idct)
+        amdahl = amdahl_rows(images, wl, world, pg, amdahl_n(args, wl), row0, n_rows, args.idct)
     elif not args.no_amdahl:
-        amdahl = amdahl_run(images, wl, world, pg, args.amdahl_images, idct=args.idct)
+        amdahl = amdahl_run(images, wl, world, pg, amdahl_n(args, wl), idct=args.idct)
         # the same with one host core left to the GPU submission thread and
         # the driver (both legs on the remaining cores): all-cores Huffman
         # is fastest, but its workers then get preempted by the pipeline
         cores = len(os.sched_getaffinity(0)) // world
         if cores > 2:
-            r = amdahl_run(images, wl, world, pg, args.amdahl_images, reserve=1, idct=args.idct)
+            r = amdahl_run(images, wl, world, pg, amdahl_n(args, wl), reserve=1, idct=args.idct)
             amdahl["one_core_reserved"] = {k: r[k] for k in ("t_huff_ms", "t_wall_ms", "frac_of_bound",
                                                              "mpix_s", "host_threads_per_rank")}
 
