@@ -1437,7 +1437,9 @@ __device__ __forceinline__ bool tc_stage(const int16_t *__restrict__ src, uint8_
     for (int k = 0; k < 4; ++k)
         sts128(arow_tile + tc::kmaj(row, 16 * k), make_uint4(lo[4 * k], lo[4 * k + 1], lo[4 * k + 2], lo[4 * k + 3]));
     const int dc = (int)(short)(raw[0].x & 0xffff);
-    const float dcq = fabsf((float)dc * (float)q0);  // exact: |dc q0| < 2^31 fits 24 bits? bounded below
+    // |dc q0| < 2^31; the float product is within 2^-24 relative, covered by
+    // the (1 + 2^-23) factors where it enters the bounds
+    const float dcq = fabsf((float)dc * (float)q0);
     const float nrm = __fsqrt_ru((float)n2);
     const float scale = __int_as_float((127 + F) << 23);  // 2^F
     const float eu = __fmul_ru(__fmaf_ru(nrm, dd, __fmul_ru(__fmul_ru(dcq, 1.0000001f), 0x1p-44f)), scale);
