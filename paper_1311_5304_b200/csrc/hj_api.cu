@@ -123,22 +123,24 @@ static int64_t strips_of(int mpr, int S, int sub) {
     return (mpr + S - 1) / S;
 }
 
-// Launch group of an image: the float64 AAN path runs on the FP32-screen
-// kernel (kKindSimt, v3) - or, with HJ_RENDER_TC=1 in the environment, on the
-// tensor-core screen kernel (kKindTc, v4: bit-exact, 0.54x the v3 rate on
-// the B200); direct (kKindDirect) and islow (kKindIslow)
-// have their own groups.
-static bool tc_enabled() {
-    static const bool on = [] {
+// Launch group of an image.  The reference's float64 arithmetic has two
+// kernels: AAN ("fast") runs on the FP32-screen kernel
+// (kKindSimt, v3), which is faster there; the direct basis runs on the
+// tensor-core screen kernel (kKindTc, v4), which proves >99 % of its blocks
+// where v3 sends every block to exact float64.  HJ_RENDER_TC=1 puts both on
+// v4, HJ_RENDER_TC=0 both on v3 (kKindDirect).  islow (kKindIslow) has its
+// own kernel variant.
+static int tc_mode() {
+    static const int m = [] {
         const char *v = std::getenv("HJ_RENDER_TC");
-        return v && v[0] && v[0] != '0';
+        return v && v[0] ? (v[0] != '0' ? 1 : 0) : -1;
     }();
-    return on;
+    return m;
 }
 static int idct_kind(const hj_image_t &im) {
     if (im.flags & HJ_FLAG_ISLOW_IDCT) return hj::kKindIslow;
-    if (im.flags & HJ_FLAG_DIRECT_IDCT) return hj::kKindDirect;
-    return tc_enabled() ? hj::kKindTc : hj::kKindSimt;
+    if (im.flags & HJ_FLAG_DIRECT_IDCT) return tc_mode() == 0 ? hj::kKindDirect : hj::kKindTc;
+    return tc_mode() == 1 ? hj::kKindTc : hj::kKindSimt;
 }
 
 int choose_rows_per_tile(const hj_image_t *images, int n, int sub, int kind, int S, int64_t slots) {

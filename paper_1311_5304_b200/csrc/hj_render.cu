@@ -1290,6 +1290,7 @@ struct Dims {
 }  // namespace tcs
 
 __device__ const double kMtab[64 * 64] = HJ_MTAB_INIT;
+__device__ const double kMtabDirect[64 * 64] = HJ_MTAB_DIRECT_INIT;  // idct="direct"
 
 template <int SUB>
 struct SmemTc {
@@ -1322,6 +1323,7 @@ struct SmemTc {
     float dd[2], gg[2];                           // per table: error and magnitude factors
     unsigned long long mx[2], dmax[2], gmax[2];   // reductions (positive doubles as bits)
     int cr_differs;                               // Cr table != Cb table
+    double dcc;                                   // the DC column's constant (M[0][i], all i)
 };
 
 // Build B (3 limbs of round(2^F M q), canonical K-major) for the luma table
@@ -1332,6 +1334,10 @@ __device__ __forceinline__ void tc_build_b(SmemTc<SUB> &sm, const hj_image_t &im
     const int tid = threadIdx.x;
     const int c = tid >> 6, i = tid & 63;
     const int *q = im.q + (c ? 64 : 0);
+    // the AAN map (fast) or the direct-basis map (idct="direct"); their DC
+    // columns are constants (exactly 1/8 for AAN) and enter through the bias
+    const double *kMtab = (im.flags & HJ_FLAG_DIRECT_IDCT) ? ::hj::kMtabDirect : ::hj::kMtab;
+    if (tid == 0) sm.dcc = kMtab[0];
     if (tid < 2) sm.mx[tid] = sm.dmax[tid] = sm.gmax[tid] = 0ull;
     if (tid == 0) sm.cr_differs = 0;
     __syncthreads();
@@ -1412,7 +1418,7 @@ __device__ __forceinline__ int tc_y_off(int b) {
 // Stage one block: int8 row of the operand tile, bias / bound, range guard.
 // Returns true when the block must take the exact path.
 __device__ __forceinline__ bool tc_stage(const int16_t *__restrict__ src, uint8_t *arow_tile, int row, int q0,
-                                         int F, float dd, float gg, bool direct, int2 &meta) {
+                                         int F, float dd, float gg, double dcc, bool bad_in, int2 &meta) {
     int4 raw[8];
     const int4 *s4 = reinterpret_cast<const int4 *>(src);
 #pragma unroll
@@ -1443,13 +1449,15 @@ __device__ __forceinline__ bool tc_stage(const int16_t *__restrict__ src, uint8_
     const float nrm = __fsqrt_ru((float)n2);
     const float scale = __int_as_float((127 + F) << 23);  // 2^F
     const float eu = __fmul_ru(__fmaf_ru(nrm, dd, __fmul_ru(__fmul_ru(dcq, 1.0000001f), 0x1p-44f)), scale);
-    const int e = (int)ceilf(eu) + 2;
+    const int e = (int)ceilf(eu) + 3;  // + the bias rounding below
     // no-wrap guard: |T|, |T + 2e| < 2^31 with |s| <= |dc q0| / 8 + ||c_AC|| G
     const float sb = __fmaf_ru(nrm, gg, __fmul_ru(__fmul_ru(dcq, 1.0000001f), 0.125f));
     const bool wrap = __fadd_ru(__fmul_ru(__fadd_ru(sb, 129.0f), scale), 2.0f * (float)e + 8.0f) >= 2.0e9f;
-    const long long bias = ((257ll << F) >> 1) - e + (((long long)dc * q0) << F >> 3);
+    // 2^F (128.5 + dcc dc q0), rounded: dcc = 1/8 (AAN, exact) or the direct
+    // basis' T00^2 (its double and this product err < 2^-24 absolute)
+    const long long bias = __double2ll_rn(ldexp(fma(dcc, (double)dc * (double)q0, 128.5), F)) - e;
     meta = make_int2((int)bias, 2 * e);
-    return direct || rng != 0 || wrap;
+    return bad_in || rng != 0 || wrap;
 }
 
 template <int SUB>
@@ -1467,6 +1475,8 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int mpr = im.mcus_per_row;
     const int S = t.m1 - t.m0;
+    // idct="direct" is screened too (its own exact map); the exact path
+    // below still recomputes unproven blocks with the direct basis
     const bool direct = (im.flags & HJ_FLAG_DIRECT_IDCT) != 0;
     for (int i = tid; i < 192; i += NT) sm.qi[i >> 6][i & 63] = im.q[i];
     if (tid == 0) {
@@ -1486,6 +1496,7 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
     const int F0 = sm.F[0], F1 = sm.F[1];
     const float dd0 = sm.dd[0], dd1 = sm.dd[1], gg0 = sm.gg[0], gg1 = sm.gg[1];
     const bool cr_exact = sm.cr_differs != 0;
+    const double dcc = sm.dcc;
 
     const int cm_lo = (SUB == HJ_SUB_444) ? t.m0 : t.m0 - 1;
     const int n_cm = (SUB == HJ_SUB_444) ? S : S + 2;
@@ -1534,7 +1545,7 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
             if (j < n_y) {
                 int2 meta;
                 const bool bad = tc_stage(im.y + (yblk0 + j) * 64, sm.a.ay[j >> 7], j & 127, sm.qi[0][0], F0, dd0,
-                                          gg0, direct, meta);
+                                          gg0, dcc, false, meta);
                 sm.meta[j] = meta;
                 sm.flag[j] = bad;
                 if (bad) {
@@ -1552,7 +1563,7 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
                 const int64_t cblk = (int64_t)crow * mpr + m;
                 int2 meta;
                 const bool bad = tc_stage((k ? im.cr : im.cb) + cblk * 64, k ? sm.a.acr : sm.a.acb, lm, sm.qi[1 + k][0],
-                                          F1, dd1, gg1, direct || (k && cr_exact), meta);
+                                          F1, dd1, gg1, dcc, k && cr_exact, meta);
                 sm.meta[D::NY + k * D::NC + lm] = meta;
                 sm.flag[D::NY + k * D::NC + lm] = bad;
                 uint32_t dst;
