@@ -1,9 +1,11 @@
-"""The tensor-core IDCT screen (render_tc_kernel, opt-in: HJ_RENDER_TC=1;
-DESIGN.md §3.5) under the whole GPU parity suite: every golden case (AAN and
-direct), partial row ranges, concurrent threads, BASELINE sizes vs the oracle,
-adversarial int16 coefficients (out-of-range AC, huge DC: the exact path),
-mixed-subsampling device batches, MCU-row shards and strip sweeps - bit-exact
-RGB, in a subprocess because the switch is read once per process."""
+"""The tensor-core IDCT screen (render_tc_kernel) under the
+whole GPU parity suite with HJ_RENDER_TC=1 (AAN images on it too; by default
+only idct="direct" runs on it, covered by the default suite's direct cases):
+every golden case (AAN and direct), partial row ranges, concurrent threads,
+BASELINE sizes vs the oracle, adversarial int16 coefficients (out-of-range AC,
+huge DC, Cb and Cr tables that differ: the exact path), mixed-subsampling
+device batches, MCU-row shards and strip sweeps - bit-exact RGB, in a
+subprocess because the switch is read once per process."""
 import os
 import subprocess
 import sys
