@@ -163,6 +163,25 @@ def test_full_size_against_oracle(w, h, q, sub, kw):
     assert np.array_equal(px.data, want)
 
 
+@pytest.mark.parametrize("w,h,q,sub,kw", [
+    (1920, 1080, 90, "420", {}),
+    (1001, 999, 80, "420", {}),
+    (1925, 300, 60, "422", {"restart_blocks": 7}),
+    (1922, 700, 70, "444", {}),
+], ids=["1080p_420", "odd_420", "w1mod4_422_rst", "w2mod4_444"])
+def test_direct_idct_full_size_against_oracle(w, h, q, sub, kw):
+    """idct="direct" at BASELINE-like sizes: by default these images run on the
+    tensor-core screen kernel - its exact direct-basis map,
+    the rounded T00^2 DC bias and the exact fallback against the oracle."""
+    from paper_1311_5304_b200.block_transforms import alloc_pixels, render_rows
+    p, coeffs, qt = _synthetic(w, h, q, sub, **kw)
+    px = alloc_pixels(w, h)
+    render_rows(coeffs, qt, px, 0, coeffs.geometry.mcu_rows, fast=False)
+    want = oracle.render(coeffs.y_blocks, coeffs.cb_blocks, coeffs.cr_blocks, qt, w, h,
+                         {"444": 0, "422": 1, "420": 2}[sub], False, threads=16)
+    assert np.array_equal(px.data, want)
+
+
 @pytest.mark.parametrize("sub", [0, 1, 2])
 def test_adversarial_coefficients(cuda, sub):
     """Extreme int16 coefficients, q up to 255 (saturation on both ends),
