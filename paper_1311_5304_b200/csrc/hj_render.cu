@@ -1032,7 +1032,7 @@ template <int SUB, int MODE>
 __global__ void __launch_bounds__(kNT<SUB>, ctas_per_sm(SUB))
 render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ tiles) {
     using G = Geo<SUB>;
-    extern __shared__ __align__(16) uint8_t smem_raw[];
+    extern __shared__ __align__(1024) uint8_t smem_raw[];  // (one declaration for both kernels)
     Smem<SUB> &sm = *reinterpret_cast<Smem<SUB> *>(smem_raw);
 
     const Tile t = tiles[blockIdx.x];
@@ -1042,12 +1042,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
     const int S = t.m1 - t.m0;
     const bool direct = MODE == kModeRef && (im.flags & HJ_FLAG_DIRECT_IDCT) != 0;
     constexpr bool kIslow = MODE == kModeIslow;
-    // islow: real chroma size (libjpeg downsampled_width / _height) and box
-    // replication instead of the triangle filter when it is <= 2 columns wide
-    const int lj_cw = (im.width + 1) >> 1, lj_ch = (im.height + 1) >> 1;
-    const bool lj_box = kIslow && lj_cw <= 2;
     constexpr int kThreads = kNT<SUB>;
-    constexpr int kExactGroups = ::hj::kExactGroups<SUB>;
     for (int i = tid; i < 192; i += kThreads) {
         const int q = im.q[i];
         sm.qi[i >> 6][i & 63] = q;
@@ -1061,7 +1056,6 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
     const int n_cm = (SUB == HJ_SUB_444) ? S : S + 2;
     // Y jobs (two blocks): 444 MCU pair; 422 one MCU; 420 half MCU
     const int n_yj = (SUB == HJ_SUB_444) ? (S + 1) / 2 : (SUB == HJ_SUB_422 ? S : 2 * S);
-    const bool left_edge = (t.m0 == 0), right_edge = (t.m1 == mpr);
     constexpr int YB = G::MW / 8 * (G::MH / 8);          // Y blocks per MCU
     const int mcu_rows = im.mcu_rows;
     __syncthreads();
