@@ -45,6 +45,7 @@ void build_table(const hj_scan_tables_t *s, int slot, Table &t, bool ac) {
     std::memcpy(t.symbols, s->symbols[slot], sizeof(t.symbols));
     std::memset(t.look, 0, sizeof(t.look));
     std::memset(t.fast, 0, sizeof(t.fast));
+    std::memset(t.pair, 0, sizeof(t.pair));
     // every code of <= kLook bits owns the 2^(kLook - len) lookahead values it prefixes
     for (int len = 1; len <= kLook; ++len) {
         if (t.maxcode[len] < 0) continue;
@@ -75,6 +76,25 @@ void build_table(const hj_scan_tables_t *s, int slot, Table &t, bool ac) {
                 t.fast[v] = e;
             }
         }
+    }
+    if (!ac) return;
+    // pairs: a complete first coefficient (kCoef with a nonzero size) whose
+    // remaining lookahead bits hold a complete second one
+    for (int v = 0; v < (1 << kLook); ++v) {
+        const uint32_t e1 = t.fast[v];
+        if (((e1 >> 25) & 7) != kCoef || (e1 >> 28) == 0) continue;
+        const int l1 = (e1 >> 20) & 31;
+        const int rest = kLook - l1;
+        if (rest <= 0) continue;
+        const uint32_t e2 = t.fast[(v << l1) & ((1 << kLook) - 1)];
+        const uint32_t k2 = (e2 >> 25) & 7;
+        if (k2 != kCoef && k2 != kEob) continue;
+        const int l2 = (e2 >> 20) & 31;
+        if (l2 > rest) continue;  // the second code / magnitude needs bits past the lookahead
+        const int v1 = (int16_t)(e1 & 0xffff), v2 = k2 == kEob ? 0 : (int16_t)(e2 & 0xffff);
+        if (v1 < -512 || v1 > 511 || v2 < -512 || v2 > 511) continue;
+        t.pair[v] = ((uint32_t)v1 & 1023) | ((uint32_t)v2 & 1023) << 10 | ((e1 >> 16) & 15) << 20 |
+                    (k2 == kEob ? 0u : ((e2 >> 16) & 15) << 24) | (uint32_t)(l1 + l2) << 28;
     }
 }
 

@@ -45,9 +45,16 @@ constexpr int kLook = 11;
 // (code + magnitude), 25-27 kind, 28-31 code length.
 enum Kind : uint32_t { kSlow = 0, kCoef = 1, kEob = 2, kZrl = 3, kCodeOnly = 4 };
 
+// pair[] entry (AC tables, whole-scan decoder): two consecutive AC
+// coefficients whose codes and magnitudes both lie inside the 11-bit
+// lookahead.  bits 0-9 value 1, 10-19 value 2 (signed; 0 = the second
+// symbol is the block's EOB), 20-23 run 1, 24-27 run 2, 28-31 bits consumed
+// by both (0 = no pair: fall back to fast[]).  (q90 symbols average ~5 bits
+// with their magnitudes.)
 struct Table {
     uint16_t look[1 << kLook];  // (len << 8) | symbol, len 0 = code longer than kLook
     uint32_t fast[1 << kLook];
+    uint32_t pair[1 << kLook];
     int32_t mincode[17], maxcode[17], valptr[17];
     uint8_t symbols[256];
 };
@@ -223,6 +230,26 @@ inline int decode_block(Reader &br, const Table &dc, const Table &ac, int16_t *o
     while (k < 64) {
         if (br.nbits < 32) br.refill();
         if (kTrack) tr->need_hi = br.consumed() + 8;
+        if (!kTrack && br.nbits >= kLook) {
+            // two coefficients per lookup when both fit the lookahead and
+            // stay inside the block (else the single-symbol path below,
+            // which also reports any error exactly)
+            const uint32_t pe = ac.pair[br.peek(kLook)];
+            const int r1 = (int)(pe >> 20) & 15, r2 = (int)(pe >> 24) & 15;
+            const int v2 = (int32_t)(pe << 12) >> 22;
+            // (an EOB pair needs room after its coefficient: a block whose
+            // coefficient 63 is coded ends there without an EOB)
+            if ((pe >> 28) != 0 && k + r1 + (v2 ? r2 + 1 : 1) <= 63) {
+                br.skip((int)(pe >> 28));
+                k += r1;
+                out[kZigzag[k]] = (int16_t)((int32_t)(pe << 22) >> 22);
+                if (!v2) break;  // coefficient + EOB
+                k += 1 + r2;
+                out[kZigzag[k]] = (int16_t)v2;
+                ++k;
+                continue;
+            }
+        }
         if (br.nbits >= kLook) {
             const uint32_t e = ac.fast[br.peek(kLook)];
             const uint32_t kind = (e >> 25) & 7;
