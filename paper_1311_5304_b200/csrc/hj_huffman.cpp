@@ -80,13 +80,15 @@ void build_table(const hj_scan_tables_t *s, int slot, Table &t, bool ac) {
     if (!ac) return;
     // pairs: a complete first coefficient (kCoef with a nonzero size) whose
     // remaining lookahead bits hold a complete second one
-    for (int v = 0; v < (1 << kLook); ++v) {
-        const uint32_t e1 = t.fast[v];
+    for (int v = 0; v < (1 << kPairLook); ++v) {
+        const uint32_t e1 = t.fast[v >> (kPairLook - kLook)];
         if (((e1 >> 25) & 7) != kCoef || (e1 >> 28) == 0) continue;
         const int l1 = (e1 >> 20) & 31;
-        const int rest = kLook - l1;
+        const int rest = kPairLook - l1;
         if (rest <= 0) continue;
-        const uint32_t e2 = t.fast[(v << l1) & ((1 << kLook) - 1)];
+        // the next kLook bits after the first coefficient (known: `rest` of them)
+        const int nxt = (int)(((uint32_t)v << l1) & ((1u << kPairLook) - 1));
+        const uint32_t e2 = t.fast[nxt >> (kPairLook - kLook)];
         const uint32_t k2 = (e2 >> 25) & 7;
         if (k2 != kCoef && k2 != kEob) continue;
         const int l2 = (e2 >> 20) & 31;

@@ -40,6 +40,10 @@ namespace hj {
 namespace huff {
 
 constexpr int kLook = 11;
+#ifndef HJ_PAIR_LOOK
+#define HJ_PAIR_LOOK 12
+#endif
+constexpr int kPairLook = HJ_PAIR_LOOK;  // lookahead of the two-symbol table
 
 // fast[] entry: bits 0-15 value (int16), 16-19 run, 20-24 bits consumed
 // (code + magnitude), 25-27 kind, 28-31 code length.
@@ -54,7 +58,7 @@ enum Kind : uint32_t { kSlow = 0, kCoef = 1, kEob = 2, kZrl = 3, kCodeOnly = 4 }
 struct Table {
     uint16_t look[1 << kLook];  // (len << 8) | symbol, len 0 = code longer than kLook
     uint32_t fast[1 << kLook];
-    uint32_t pair[1 << kLook];
+    uint32_t pair[1 << kPairLook];
     int32_t mincode[17], maxcode[17], valptr[17];
     uint8_t symbols[256];
 };
@@ -230,11 +234,11 @@ inline int decode_block(Reader &br, const Table &dc, const Table &ac, int16_t *o
     while (k < 64) {
         if (br.nbits < 32) br.refill();
         if (kTrack) tr->need_hi = br.consumed() + 8;
-        if (!kTrack && br.nbits >= kLook) {
+        if (!kTrack && br.nbits >= kPairLook) {
             // two coefficients per lookup when both fit the lookahead and
             // stay inside the block (else the single-symbol path below,
             // which also reports any error exactly)
-            const uint32_t pe = ac.pair[br.peek(kLook)];
+            const uint32_t pe = ac.pair[br.peek(kPairLook)];
             const int r1 = (int)(pe >> 20) & 15, r2 = (int)(pe >> 24) & 15;
             const int v2 = (int32_t)(pe << 12) >> 22;
             // (an EOB pair needs room after its coefficient: a block whose
