@@ -41,7 +41,7 @@ namespace huff {
 
 constexpr int kLook = 11;
 #ifndef HJ_PAIR_LOOK
-#define HJ_PAIR_LOOK 12
+#define HJ_PAIR_LOOK 13
 #endif
 constexpr int kPairLook = HJ_PAIR_LOOK;  // lookahead of the two-symbol table
 
