@@ -311,11 +311,18 @@ def port_rate(images, wl, threads, budget_s=2.0):
     return round(n * w * h / (time.perf_counter() - t0) / 1e6, 2)
 
 
-def amdahl_n(args, wl):
-    """Images per rank of the Huffman-inclusive pipeline run."""
+def amdahl_n(args, wl, world=1):
+    """Images per rank of the Huffman-inclusive pipeline run: at least 32,
+    >= 64 Mpx, and ~8 images per host thread where the batch's page-locked
+    buffers stay under ~4 GB, so pipeline fill / drain (the last images' H2D,
+    render and D2H after their Huffman) does not dominate the fraction."""
     if args.amdahl_images:
         return args.amdahl_images
-    return max(32, -(-64_000_000 // (wl[0] * wl[1])))
+    px = wl[0] * wl[1]
+    threads = max(1, len(os.sched_getaffinity(0)) // world)
+    n = max(32, -(-64_000_000 // px), min(8 * threads, 4_000_000_000 // (6 * px)))
+    # whole rounds of the host threads (no half-empty last round in either leg)
+    return max(32, n - n % threads) if n > 32 else n
 
 
 def amdahl_run(images, wl, world, pg, n_images, reserve=0, idct="fast"):
@@ -901,15 +908,15 @@ def main():
     # ---- end to end INCLUDING host Huffman: the paper's Amdahl metric
     amdahl = None
     if not args.no_amdahl and rows_mode:
-        amdahl = amdahl_rows(images, wl, world, pg, amdahl_n(args, wl), row0, n_rows, args.idct)
+        amdahl = amdahl_rows(images, wl, world, pg, amdahl_n(args, wl, world), row0, n_rows, args.idct)
     elif not args.no_amdahl:
-        amdahl = amdahl_run(images, wl, world, pg, amdahl_n(args, wl), idct=args.idct)
+        amdahl = amdahl_run(images, wl, world, pg, amdahl_n(args, wl, world), idct=args.idct)
         # the same with one host core left to the GPU submission thread and
         # the driver (both legs on the remaining cores): all-cores Huffman
         # is fastest, but its workers then get preempted by the pipeline
         cores = len(os.sched_getaffinity(0)) // world
         if cores > 2:
-            r = amdahl_run(images, wl, world, pg, amdahl_n(args, wl), reserve=1, idct=args.idct)
+            r = amdahl_run(images, wl, world, pg, amdahl_n(args, wl, world), reserve=1, idct=args.idct)
             amdahl["one_core_reserved"] = {k: r[k] for k in ("t_huff_ms", "t_wall_ms", "frac_of_bound",
                                                              "mpix_s", "host_threads_per_rank")}
 
