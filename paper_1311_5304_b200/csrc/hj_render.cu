@@ -1267,9 +1267,19 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
 namespace tcs {
 constexpr int kThreads = 256;
 constexpr int kCols = 256;                 // TMEM columns per CTA
-constexpr int kBuf0 = 0, kBuf1 = 128;      // two unit buffers (96 columns each)
 constexpr int kFmax = 21;                  // |s| + 128.5 < 2^(31-F) = 1024 at F = 21
-constexpr int kHalfB = 96 * 64;            // B operand of one N=96 half (3 limbs x 32 outputs)
+// A unit = kUnitOut outputs of one operand tile: one MMA of N = 3 kUnitOut
+// (limb-stacked) per K step into one of kNBuf TMEM buffers; the MMAs run
+// kNBuf units ahead of the epilogue.
+#ifndef HJ_TC_UNIT_OUT
+#define HJ_TC_UNIT_OUT 32
+#endif
+constexpr int kUnitOut = HJ_TC_UNIT_OUT;   // 32 or 16
+constexpr int kParts = 64 / kUnitOut;      // units per operand tile
+constexpr int kUnitN = 3 * kUnitOut;       // MMA N (TMEM columns per unit)
+constexpr int kNBuf = kCols / kUnitN;      // 2 (N = 96) or 5 (N = 48)
+constexpr int kPartB = kUnitN * 64;        // B operand bytes of one unit's outputs
+constexpr int kNS = kUnitOut / 2;          // samples per thread per unit (two warps per lane quadrant)
 template <int SUB>
 constexpr int kStrip = SUB == HJ_SUB_444 ? 96 : SUB == HJ_SUB_422 ? 64 : 48;
 template <int SUB>
@@ -1298,7 +1308,7 @@ struct SmemTc {
         } a;                                      // MMA A operands (phase A)
         double g[tcs::kThreads / 8][64];          // exact-path staging (phase B)
     };
-    alignas(128) uint8_t bm[2][2 * tcs::kHalfB];  // MMA B: [Y, chroma] x two N=96 halves (limb-stacked)
+    alignas(128) uint8_t bm[2][tcs::kParts * tcs::kPartB];  // MMA B: [Y, chroma] x parts (limb-stacked)
     alignas(16) uint8_t ys[G::YSLOTS][G::MH * G::YW];
     alignas(16) uint8_t cbp[SUB == HJ_SUB_444 ? 2 : 1][SUB == HJ_SUB_444 ? 8 * G::YW : 16];
     alignas(16) uint8_t crp[SUB == HJ_SUB_444 ? 2 : 1][SUB == HJ_SUB_444 ? 8 * G::YW : 16];
@@ -1310,8 +1320,8 @@ struct SmemTc {
     uint32_t qdst[2][D::NB];
     int n_queue[2];
     int n_taken[2];
-    alignas(8) uint64_t full[2];
-    alignas(8) uint64_t empty[2];
+    alignas(8) uint64_t full[tcs::kNBuf];
+    alignas(8) uint64_t empty[tcs::kNBuf];
     uint32_t tmem;
     int F[2];
     float dd[2], gg[2];                           // per table: error and magnitude factors
@@ -1347,10 +1357,11 @@ __device__ __forceinline__ void tc_build_b(SmemTc<SUB> &sm, const hj_image_t &im
         if (mx > 0.0) F = min(F, (int)floor(log2(8355711.0 / mx)));  // balanced 3-limb range
         const double sc = ldexp(1.0, F), isc = ldexp(1.0, -F);
         double dsum = 0.0, gsum = 0.0;
-        // output i of half h = i >> 5 is row 32 d + (i & 31) of that half's
-        // N = 96 operand, d = limb: one MMA yields all three limb products
-        uint8_t *bh = sm.bm[c] + (i >> 5) * tcs::kHalfB;
-        const int r0 = i & 31;
+        // output i of part p = i / kUnitOut is row kUnitOut d + (i % kUnitOut)
+        // of that part's N = 3 kUnitOut operand, d = limb: one MMA yields all
+        // three limb products
+        uint8_t *bh = sm.bm[c] + (i / tcs::kUnitOut) * tcs::kPartB;
+        const int r0 = i % tcs::kUnitOut;
         for (int j0 = 0; j0 < 64; j0 += 4) {
             uint32_t w0 = 0, w1 = 0, w2 = 0;
 #pragma unroll
@@ -1374,8 +1385,8 @@ __device__ __forceinline__ void tc_build_b(SmemTc<SUB> &sm, const hj_image_t &im
                 w2 |= (uint32_t)(l2 & 255) << (8 * k);
             }
             *reinterpret_cast<uint32_t *>(bh + tc::kmaj(r0, j0)) = w0;
-            *reinterpret_cast<uint32_t *>(bh + tc::kmaj(32 + r0, j0)) = w1;
-            *reinterpret_cast<uint32_t *>(bh + tc::kmaj(64 + r0, j0)) = w2;
+            *reinterpret_cast<uint32_t *>(bh + tc::kmaj(tcs::kUnitOut + r0, j0)) = w1;
+            *reinterpret_cast<uint32_t *>(bh + tc::kmaj(2 * tcs::kUnitOut + r0, j0)) = w2;
         }
         atomicMax(&sm.dmax[c], (unsigned long long)__double_as_longlong(sqrt(dsum)));
         atomicMax(&sm.gmax[c], (unsigned long long)__double_as_longlong(sqrt(gsum)));
@@ -1475,10 +1486,10 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
     for (int i = tid; i < 192; i += NT) sm.qi[i >> 6][i & 63] = im.q[i];
     if (tid == 0) {
         sm.n_queue[0] = sm.n_queue[1] = sm.n_taken[0] = sm.n_taken[1] = 0;
-        tc::mbar_init(&sm.full[0], 1);
-        tc::mbar_init(&sm.full[1], 1);
-        tc::mbar_init(&sm.empty[0], NT / 32);
-        tc::mbar_init(&sm.empty[1], NT / 32);
+        for (int b = 0; b < tcs::kNBuf; ++b) {
+            tc::mbar_init(&sm.full[b], 1);
+            tc::mbar_init(&sm.empty[b], NT / 32);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     if (warp == 0) tc::tmem_alloc<tcs::kCols>(&sm.tmem);
@@ -1497,7 +1508,7 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
     const int n_yb = (SUB == HJ_SUB_444) ? S : (SUB == HJ_SUB_422 ? 2 * S : 4 * S);
     constexpr int YB = G::MW / 8 * (G::MH / 8);
     const int mcu_rows = im.mcu_rows;
-    uint32_t unit = 0;  // running unit counter (TMEM buffer = unit & 1)
+    uint32_t unit = 0;  // running unit counter (TMEM buffer = unit % kNBuf)
 
     const int s_begin = (SUB == HJ_SUB_420) ? max(t.r0 - 2, -1) : t.r0;
     const int s_end = t.r1;
@@ -1581,49 +1592,54 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
         __syncthreads();
 
         // ---------------- units: MMA (thread 0) -> TMEM -> proven samples
-        const int n_yunits = do_y ? 2 * ((n_yb + 127) >> 7) : 0;
-        const int n_units = n_yunits + (do_c ? 4 : 0);
+        constexpr int P = tcs::kParts, NS = tcs::kNS;
+        const int n_yunits = do_y ? P * ((n_yb + 127) >> 7) : 0;
+        const int n_units = n_yunits + (do_c ? 2 * P : 0);
+        // Y unit k: tile k / P, part k % P; chroma unit: (Cb, Cr) x part, order Cb0 Cr0 Cb1 Cr1 ...
         auto issue = [&](int k, uint32_t u) {
-            const uint32_t b = u & 1, dcol = tbase + (b ? tcs::kBuf1 : tcs::kBuf0);
-            if (u >= 2) tc::mbar_wait(&sm.empty[b], ((u - 2) >> 1) & 1);
+            const uint32_t b = u % tcs::kNBuf, dcol = tbase + b * tcs::kUnitN;
+            if (u >= (uint32_t)tcs::kNBuf) tc::mbar_wait(&sm.empty[b], ((u - tcs::kNBuf) / tcs::kNBuf) & 1);
             tc::fence_after();
-            constexpr uint32_t id = tc::idesc_i8(96, true, true);
-            // Y unit k: tile k >> 1, half k & 1; chroma unit: (Cb, Cr) x half, order Cb0 Cr0 Cb1 Cr1
+            constexpr uint32_t id = tc::idesc_i8(tcs::kUnitN, true, true);
             const int cu = k - n_yunits;
-            const uint32_t a0 = k < n_yunits ? tc::smem_u32(sm.a.ay[k >> 1]) : tc::smem_u32((cu & 1) ? sm.a.acr : sm.a.acb);
-            const uint32_t b0 = tc::smem_u32(sm.bm[k < n_yunits ? 0 : 1]) + (k < n_yunits ? (k & 1) : (cu >> 1)) * tcs::kHalfB;
+            const uint32_t a0 = k < n_yunits ? tc::smem_u32(sm.a.ay[k / P]) : tc::smem_u32((cu & 1) ? sm.a.acr : sm.a.acb);
+            const uint32_t b0 = tc::smem_u32(sm.bm[k < n_yunits ? 0 : 1]) + (k < n_yunits ? k % P : cu >> 1) * tcs::kPartB;
 #pragma unroll
             for (int ks = 0; ks < 2; ++ks) tc::mma_i8(dcol, tc::sdesc(a0 + ks * 256), tc::sdesc(b0 + ks * 256), id, ks);
             tc::commit(&sm.full[b]);
         };
-        if (tid == 0) {
-            if (n_units > 0) issue(0, unit);
-            if (n_units > 1) issue(1, unit + 1);
-        }
+        if (tid == 0)
+            for (int k = 0; k < n_units && k < tcs::kNBuf; ++k) issue(k, unit + k);
         const int qd = warp & 3, grp = warp >> 2;
         const int row = 32 * qd + lane;
-        uint32_t cbk[4] = {0, 0, 0, 0};  // 4:2:x: Cb samples held for the paired Cr unit
+        uint32_t cbk[NS / 4];  // 4:2:x: Cb samples held for the paired Cr unit
 #pragma unroll 1
         for (int k = 0; k < n_units; ++k, ++unit) {
-            const uint32_t b = unit & 1;
-            const uint32_t tl = tbase + ((uint32_t)(32 * qd) << 16) + (b ? tcs::kBuf1 : tcs::kBuf0);
-            tc::mbar_wait(&sm.full[b], (unit >> 1) & 1);
+            const uint32_t b = unit % tcs::kNBuf;
+            const uint32_t tl = tbase + ((uint32_t)(32 * qd) << 16) + b * tcs::kUnitN;
+            tc::mbar_wait(&sm.full[b], (unit / tcs::kNBuf) & 1);
             tc::fence_after();
             __syncwarp();  // the tcgen05.ld below are warp-collective (.sync.aligned)
-            uint32_t a0[16], a1[16], a2[16];  // limbs 0..2 of this thread's 16 outputs
-            tc::ld16(tl + 16 * grp, a0);
-            tc::ld16(tl + 32 + 16 * grp, a1);
-            tc::ld16(tl + 64 + 16 * grp, a2);
+            uint32_t a0[NS], a1[NS], a2[NS];  // limbs 0..2 of this thread's NS outputs
+            if constexpr (NS == 16) {
+                tc::ld16(tl + 16 * grp, a0);
+                tc::ld16(tl + tcs::kUnitOut + 16 * grp, a1);
+                tc::ld16(tl + 2 * tcs::kUnitOut + 16 * grp, a2);
+            } else {
+                tc::ld8(tl + NS * grp, a0);
+                tc::ld8(tl + tcs::kUnitOut + NS * grp, a1);
+                tc::ld8(tl + 2 * tcs::kUnitOut + NS * grp, a2);
+            }
             tc::wait_ld();
             tc::fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&sm.empty[b]);
-            if (tid == 0 && k + 2 < n_units) issue(k + 2, unit + 2);
-            // this thread's block (TMEM lane) and its two sample rows 4h + 2 grp (+1)
+            if (tid == 0 && k + tcs::kNBuf < n_units) issue(k + tcs::kNBuf, unit + tcs::kNBuf);
+            // this thread's block (TMEM lane) and its NS / 8 sample rows
             const bool is_y = k < n_yunits;
             const int cu = k - n_yunits, cc = cu & 1;
-            const int h = is_y ? (k & 1) : (cu >> 1);
-            const int yb = (k >> 1) * 128 + row, lm = row;
+            const int part = is_y ? (k % P) : (cu >> 1);
+            const int yb = (k / P) * 128 + row, lm = row;
             const int fi = is_y ? yb : D::NY + cc * D::NC + lm;
             const bool valid = is_y ? yb < n_yb : (lm < n_cm && cm_lo + lm >= 0 && cm_lo + lm < mpr);
             if (valid) {
@@ -1631,33 +1647,35 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
                 const int flagged = sm.flag[fi];
                 const int2 mt = sm.meta[fi];
                 uint32_t fail = 0;
-                int n[16];
+                int n[NS];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
+                for (int i = 0; i < NS; ++i) {
                     const uint32_t T = a0[i] + (uint32_t)mt.x + (a1[i] << 8) + (a2[i] << 16);
                     fail |= T ^ (T + (uint32_t)mt.y);
                     n[i] = (int)T >> Fk;
                 }
-                const uint32_t w0 = pack4(n[0], n[1], n[2], n[3]), w1 = pack4(n[4], n[5], n[6], n[7]);
-                const uint32_t w2 = pack4(n[8], n[9], n[10], n[11]), w3 = pack4(n[12], n[13], n[14], n[15]);
-                const int srow = 4 * h + 2 * grp;
+                uint32_t w[NS / 4];
+#pragma unroll
+                for (int q = 0; q < NS / 4; ++q) w[q] = pack4(n[4 * q], n[4 * q + 1], n[4 * q + 2], n[4 * q + 3]);
+                const int srow = part * (tcs::kUnitOut / 8) + grp * (NS / 8);
                 const int cslot = (SUB == HJ_SUB_420) ? (crow % 3) : par;
-                if (is_y) {
-                    uint8_t *dst = sm.ys[par] + tc_y_off<SUB, G>(yb) + srow * G::YW;
-                    *reinterpret_cast<uint2 *>(dst) = make_uint2(w0, w1);
-                    *reinterpret_cast<uint2 *>(dst + G::YW) = make_uint2(w2, w3);
-                } else if (SUB == HJ_SUB_444) {
-                    uint8_t *dst = (cc ? sm.crp[par] : sm.cbp[par]) + 8 * lm + srow * G::YW;
-                    *reinterpret_cast<uint2 *>(dst) = make_uint2(w0, w1);
-                    *reinterpret_cast<uint2 *>(dst + G::YW) = make_uint2(w2, w3);
+                if (is_y || SUB == HJ_SUB_444) {
+                    uint8_t *dst = (is_y ? sm.ys[par] + tc_y_off<SUB, G>(yb) : (cc ? sm.crp[par] : sm.cbp[par]) + 8 * lm) +
+                                   srow * G::YW;
+#pragma unroll
+                    for (int r = 0; r < NS / 8; ++r)
+                        *reinterpret_cast<uint2 *>(dst + r * G::YW) = make_uint2(w[2 * r], w[2 * r + 1]);
                 } else if (cc == 0) {
-                    cbk[0] = w0, cbk[1] = w1, cbk[2] = w2, cbk[3] = w3;  // paired with the Cr unit next
+#pragma unroll
+                    for (int q = 0; q < NS / 4; ++q) cbk[q] = w[q];  // paired with the Cr unit next
                 } else {
                     uint16_t *cdst = &sm.cs[0][0] + cslot * 8 * G::CW + 8 * lm + srow * G::CW;
-                    sts128(cdst, make_uint4(__byte_perm(cbk[0], w0, 0x5140), __byte_perm(cbk[0], w0, 0x7362),
-                                            __byte_perm(cbk[1], w1, 0x5140), __byte_perm(cbk[1], w1, 0x7362)));
-                    sts128(cdst + G::CW, make_uint4(__byte_perm(cbk[2], w2, 0x5140), __byte_perm(cbk[2], w2, 0x7362),
-                                                    __byte_perm(cbk[3], w3, 0x5140), __byte_perm(cbk[3], w3, 0x7362)));
+#pragma unroll
+                    for (int r = 0; r < NS / 8; ++r)
+                        sts128(cdst + r * G::CW,
+                               make_uint4(__byte_perm(cbk[2 * r], w[2 * r], 0x5140), __byte_perm(cbk[2 * r], w[2 * r], 0x7362),
+                                          __byte_perm(cbk[2 * r + 1], w[2 * r + 1], 0x5140),
+                                          __byte_perm(cbk[2 * r + 1], w[2 * r + 1], 0x7362)));
                 }
                 if (!flagged && (fail >> Fk) != 0 && atomicExch(&sm.flag[fi], 1) == 0) {
                     if (is_y) {

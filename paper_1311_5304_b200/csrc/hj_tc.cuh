@@ -73,7 +73,7 @@ __device__ __forceinline__ void tmem_free(uint32_t base) {
 }
 
 // 32 lanes x 32 bit, 16 / 8 consecutive columns per thread (its own lane)
-__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&v)[16]) {
+__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t *v) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
