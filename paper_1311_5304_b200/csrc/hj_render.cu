@@ -1270,14 +1270,16 @@ constexpr int kCols = 256;                 // TMEM columns per CTA
 constexpr int kFmax = 21;                  // |s| + 128.5 < 2^(31-F) = 1024 at F = 21
 // A unit = kUnitOut outputs of one operand tile: one MMA of N = 3 kUnitOut
 // (limb-stacked) per K step into one of kNBuf TMEM buffers; the MMAs run
-// kNBuf units ahead of the epilogue.
+// kNBuf units ahead of the epilogue.  Fewer, larger units win (per-unit
+// handshake and index overhead): 64 outputs (N = 192, one buffer released
+// by the epilogue's last TMEM load) > 32 (N = 96 x 2) by 11 % > 16 (x 5).
 #ifndef HJ_TC_UNIT_OUT
-#define HJ_TC_UNIT_OUT 32
+#define HJ_TC_UNIT_OUT 64
 #endif
-constexpr int kUnitOut = HJ_TC_UNIT_OUT;   // 32 or 16
+constexpr int kUnitOut = HJ_TC_UNIT_OUT;   // 64, 32 or 16
 constexpr int kParts = 64 / kUnitOut;      // units per operand tile
 constexpr int kUnitN = 3 * kUnitOut;       // MMA N (TMEM columns per unit)
-constexpr int kNBuf = kCols / kUnitN;      // 2 (N = 96) or 5 (N = 48)
+constexpr int kNBuf = kCols / kUnitN;      // 1 (N = 192), 2 (N = 96) or 5 (N = 48)
 constexpr int kPartB = kUnitN * 64;        // B operand bytes of one unit's outputs
 constexpr int kNS = kUnitOut / 2;          // samples per thread per unit (two warps per lane quadrant)
 template <int SUB>
@@ -1620,63 +1622,75 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
             tc::mbar_wait(&sm.full[b], (unit / tcs::kNBuf) & 1);
             tc::fence_after();
             __syncwarp();  // the tcgen05.ld below are warp-collective (.sync.aligned)
-            uint32_t a0[NS], a1[NS], a2[NS];  // limbs 0..2 of this thread's NS outputs
-            if constexpr (NS == 16) {
-                tc::ld16(tl + 16 * grp, a0);
-                tc::ld16(tl + tcs::kUnitOut + 16 * grp, a1);
-                tc::ld16(tl + 2 * tcs::kUnitOut + 16 * grp, a2);
-            } else {
-                tc::ld8(tl + NS * grp, a0);
-                tc::ld8(tl + tcs::kUnitOut + NS * grp, a1);
-                tc::ld8(tl + 2 * tcs::kUnitOut + NS * grp, a2);
-            }
-            tc::wait_ld();
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&sm.empty[b]);
-            if (tid == 0 && k + tcs::kNBuf < n_units) issue(k + tcs::kNBuf, unit + tcs::kNBuf);
-            // this thread's block (TMEM lane) and its NS / 8 sample rows
+            // this thread's block (TMEM lane) and its NS / 8 sample rows,
+            // read in chunks of CH outputs (the last chunk's loads release
+            // the buffer to the next unit's MMAs)
+            constexpr int CH = NS < 16 ? NS : 16, NCH = NS / CH;
             const bool is_y = k < n_yunits;
             const int cu = k - n_yunits, cc = cu & 1;
             const int part = is_y ? (k % P) : (cu >> 1);
             const int yb = (k / P) * 128 + row, lm = row;
             const int fi = is_y ? yb : D::NY + cc * D::NC + lm;
             const bool valid = is_y ? yb < n_yb : (lm < n_cm && cm_lo + lm >= 0 && cm_lo + lm < mpr);
-            if (valid) {
-                const int Fk = is_y ? F0 : F1;
-                const int flagged = sm.flag[fi];
-                const int2 mt = sm.meta[fi];
-                uint32_t fail = 0;
-                int n[NS];
+            const int Fk = is_y ? F0 : F1;
+            const int flagged = valid ? sm.flag[fi] : 1;
+            const int2 mt = valid ? sm.meta[fi] : make_int2(0, 0);
+            const int srow0 = part * (tcs::kUnitOut / 8) + grp * (NS / 8);
+            const int cslot = (SUB == HJ_SUB_420) ? (crow % 3) : par;
+            uint32_t fail = 0;
 #pragma unroll
-                for (int i = 0; i < NS; ++i) {
+            for (int ch = 0; ch < NCH; ++ch) {
+                uint32_t a0[CH], a1[CH], a2[CH];  // limbs 0..2 of CH outputs
+                const uint32_t ta = tl + NS * grp + CH * ch;
+                if constexpr (CH == 16) {
+                    tc::ld16(ta, a0);
+                    tc::ld16(ta + tcs::kUnitOut, a1);
+                    tc::ld16(ta + 2 * tcs::kUnitOut, a2);
+                } else {
+                    tc::ld8(ta, a0);
+                    tc::ld8(ta + tcs::kUnitOut, a1);
+                    tc::ld8(ta + 2 * tcs::kUnitOut, a2);
+                }
+                tc::wait_ld();
+                if (ch == NCH - 1) {
+                    tc::fence_before();
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(&sm.empty[b]);
+                    if (tid == 0 && k + tcs::kNBuf < n_units) issue(k + tcs::kNBuf, unit + tcs::kNBuf);
+                }
+                if (!valid) continue;
+                int n[CH];
+#pragma unroll
+                for (int i = 0; i < CH; ++i) {
                     const uint32_t T = a0[i] + (uint32_t)mt.x + (a1[i] << 8) + (a2[i] << 16);
                     fail |= T ^ (T + (uint32_t)mt.y);
                     n[i] = (int)T >> Fk;
                 }
-                uint32_t w[NS / 4];
+                uint32_t w[CH / 4];
 #pragma unroll
-                for (int q = 0; q < NS / 4; ++q) w[q] = pack4(n[4 * q], n[4 * q + 1], n[4 * q + 2], n[4 * q + 3]);
-                const int srow = part * (tcs::kUnitOut / 8) + grp * (NS / 8);
-                const int cslot = (SUB == HJ_SUB_420) ? (crow % 3) : par;
+                for (int q = 0; q < CH / 4; ++q) w[q] = pack4(n[4 * q], n[4 * q + 1], n[4 * q + 2], n[4 * q + 3]);
+                const int srow = srow0 + ch * (CH / 8);
                 if (is_y || SUB == HJ_SUB_444) {
                     uint8_t *dst = (is_y ? sm.ys[par] + tc_y_off<SUB, G>(yb) : (cc ? sm.crp[par] : sm.cbp[par]) + 8 * lm) +
                                    srow * G::YW;
 #pragma unroll
-                    for (int r = 0; r < NS / 8; ++r)
+                    for (int r = 0; r < CH / 8; ++r)
                         *reinterpret_cast<uint2 *>(dst + r * G::YW) = make_uint2(w[2 * r], w[2 * r + 1]);
                 } else if (cc == 0) {
 #pragma unroll
-                    for (int q = 0; q < NS / 4; ++q) cbk[q] = w[q];  // paired with the Cr unit next
+                    for (int q = 0; q < CH / 4; ++q) cbk[ch * (CH / 4) + q] = w[q];  // paired with the Cr unit next
                 } else {
                     uint16_t *cdst = &sm.cs[0][0] + cslot * 8 * G::CW + 8 * lm + srow * G::CW;
+                    const uint32_t *cb = cbk + ch * (CH / 4);
 #pragma unroll
-                    for (int r = 0; r < NS / 8; ++r)
+                    for (int r = 0; r < CH / 8; ++r)
                         sts128(cdst + r * G::CW,
-                               make_uint4(__byte_perm(cbk[2 * r], w[2 * r], 0x5140), __byte_perm(cbk[2 * r], w[2 * r], 0x7362),
-                                          __byte_perm(cbk[2 * r + 1], w[2 * r + 1], 0x5140),
-                                          __byte_perm(cbk[2 * r + 1], w[2 * r + 1], 0x7362)));
+                               make_uint4(__byte_perm(cb[2 * r], w[2 * r], 0x5140), __byte_perm(cb[2 * r], w[2 * r], 0x7362),
+                                          __byte_perm(cb[2 * r + 1], w[2 * r + 1], 0x5140),
+                                          __byte_perm(cb[2 * r + 1], w[2 * r + 1], 0x7362)));
                 }
+            }
+            if (valid) {
                 if (!flagged && (fail >> Fk) != 0 && atomicExch(&sm.flag[fi], 1) == 0) {
                     if (is_y) {
                         push_exact(nq, queue, qdst, (uint32_t)(yblk0 + yb),
