@@ -54,3 +54,42 @@ print("ok", t1 - t0, (e1 - e0) / n_blocks)
     env = dict(os.environ, HJ_RENDER_TC="1")
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_tensor_core_extreme_tables_and_coefficients():
+    """F selection and the no-wrap guard at the table extremes: all-1 tables
+    (F capped at 21, every block near the wrap limit), all-255 tables (small
+    F, many exact-path blocks), 16-bit entries (beyond the reference's 8-bit
+    DQT; the C ABI accepts them) - AAN and direct, every subsampling, against
+    the oracle on the tensor-core kernel."""
+    code = r"""
+import numpy as np
+from paper_1311_5304_b200 import _lib
+from paper_1311_5304_b200.kernels import cuda
+from oracle import oracle
+_lib.require_device()
+t0 = _lib.lib.hj_tc_launch_count()
+rng = np.random.default_rng(7)
+fns = {0: cuda.render_rows_444, 1: cuda.render_rows_422, 2: cuda.render_rows_420}
+for sub in (0, 1, 2):
+    w, h = 97, 53
+    mw, mh, ypm = {0: (8, 8, 1), 1: (16, 8, 2), 2: (16, 16, 4)}[sub]
+    mpr, rows = -(-w // mw), -(-h // mh)
+    n_c = mpr * rows
+    for qv in (1, 255, 4000):
+        q = np.full((3, 64), qv, np.int32)
+        y = (rng.integers(-60, 60, (n_c * ypm, 64)) * (rng.random((n_c * ypm, 64)) < 0.3)).astype(np.int16)
+        y[:, 0] = rng.integers(-1024 // qv - 1, 1024 // qv + 2, n_c * ypm)
+        cb = (rng.integers(-20, 20, (n_c, 64)) * (rng.random((n_c, 64)) < 0.2)).astype(np.int16)
+        cr = cb[::-1].copy()
+        for fast in (True, False):
+            rgb = np.zeros((h, w, 3), np.uint8)
+            fns[sub](y, cb, cr, q, rgb, w, h, mpr, 0, rows, fast, True)
+            want = oracle.render(y, cb, cr, q, w, h, sub, fast)
+            assert np.array_equal(rgb, want), (sub, qv, fast)
+assert _lib.lib.hj_tc_launch_count() > t0
+print("ok")
+"""
+    env = dict(os.environ, HJ_RENDER_TC="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
