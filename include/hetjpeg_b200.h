@@ -129,11 +129,13 @@ uint64_t hj_tc_launch_count(void);
 /* Packed coefficient transfer of the synchronous drop-in (hj_render_rows*):
  * the host packs each block into a 64-bit nonzero mask of its AC coefficients,
  * a 32-bit value offset (bit 31: int16 values), its int16 DC and its nonzero AC
- * coefficients (int8 when all fit),
- * copies that, and expands it on the device - lossless; the copy is PCIe-bound
- * and 1080p q90 blocks shrink from 128 to ~46 B.  Default: on when the host CPU
- * has AVX-512 VBMI2 (HJ_PACK_H2D=0/1 overrides); mode -1 restores the default,
- * 0 forces the dense copy, 1 forces packing. */
+ * coefficients (int8 when all fit), copies that, and expands it on the device -
+ * lossless; the copy is PCIe-bound and 1080p q90 blocks shrink from 128 to
+ * ~47 B.  Default (mode -1): packed when the host CPU has AVX-512 VBMI2, >= 4
+ * calls are in flight (a saturated link), the call has <= 64k blocks and its
+ * first 4096 Y blocks pack below 0.45 of their dense bytes; otherwise dense.
+ * Mode 0 forces the dense copy, 1 forces packing; HJ_PACK_H2D=0/1 in the
+ * environment does the same.  hj_packed_h2d_active: 0 off, 1 forced, 2 auto. */
 hj_status hj_set_packed_h2d(int32_t mode);
 int32_t hj_packed_h2d_active(void);
 /* Bytes the synchronous drop-in copied host->device so far (packed or dense). */
