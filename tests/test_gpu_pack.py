@@ -51,3 +51,48 @@ def test_packed_transfer_moves_fewer_bytes():
         _lib.lib.hj_set_packed_h2d(-1)
     assert moved[0] >= dense
     assert moved[1] < 0.5 * dense, (moved, dense)
+
+
+def test_packed_transfer_concurrent_mixed_calls():
+    """8 threads calling the drop-in at once (the automatic packing policy's
+    trigger) on different sizes, subsamplings, qualities and IDCT modes - every
+    output bit-exact against the oracle."""
+    import threading
+
+    from oracle import oracle
+    from paper_1311_5304_b200 import _lib, entropy, parser
+    from paper_1311_5304_b200.block_transforms import alloc_pixels, render_rows
+    from paper_1311_5304_b200.perf_model import qtable_stack
+    from paper_1311_5304_b200.synth import synth_jpeg
+    _lib.require_device()
+    cases = []
+    rng = np.random.default_rng(11)
+    for i in range(16):
+        w, h = int(rng.integers(64, 700)), int(rng.integers(48, 500))
+        sub = ["444", "422", "420"][i % 3]
+        blob = synth_jpeg(w, h, int(rng.integers(40, 96)), sub, seed=i)
+        p = parser.parse_stream(blob)
+        co, _ = entropy.decode_all(p, blob)
+        q = qtable_stack(p)
+        fast = bool(i % 4)
+        want = oracle.render(co.y_blocks, co.cb_blocks, co.cr_blocks, q, w, h, {"444": 0, "422": 1, "420": 2}[sub], fast)
+        cases.append((co, q, w, h, fast, want))
+    errs = []
+
+    def work(k):
+        try:
+            for rep in range(3):
+                for co, q, w, h, fast, want in cases[k::8]:
+                    px = alloc_pixels(w, h)
+                    render_rows(co, q, px, 0, co.geometry.mcu_rows, fast=fast)
+                    if not np.array_equal(px.data, want):
+                        errs.append((w, h, fast))
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    b0 = _lib.lib.hj_h2d_bytes()
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(8)]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    assert not errs, errs[:3]
+    assert _lib.lib.hj_h2d_bytes() > b0
