@@ -11,9 +11,11 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -102,6 +104,14 @@ struct Plan {
     ~Plan() {
         for (auto st : side) cudaStreamDestroy(st);
         for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
+// Geometry + IDCT path of a single-image plan (the stream's plan cache).
+struct PlanKey {
+    int32_t w, h, sub, flags, row0, n_rows;
+    bool operator<(const PlanKey &o) const {
+        return std::tie(w, h, sub, flags, row0, n_rows) < std::tie(o.w, o.h, o.sub, o.flags, o.row0, o.n_rows);
     }
 };
 
@@ -1125,6 +1135,9 @@ extern "C" hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, i
 
     // submitter (this thread): the only CUDA caller
     hj_status sub_err = HJ_OK;
+    std::map<PlanKey, std::pair<std::vector<hj::Tile>, std::vector<Plan::Group>>> plan_cache;
+    std::vector<hj::Tile> tiles_buf;
+    std::vector<Plan::Group> groups_buf;
     std::vector<int> inflight;
     std::vector<int> batch;
     auto recycle = [&](bool block) {
@@ -1186,10 +1199,23 @@ extern "C" hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, i
             im.q = reinterpret_cast<const int32_t *>(misc);
             im.rgb = static_cast<uint8_t *>(sl.d_rgb);
             hj_status vs = validate(im);
-            std::vector<hj::Tile> tiles;
-            std::vector<Plan::Group> groups;
+            // tile plans depend only on the geometry and the IDCT path: a
+            // corpus of repeated sizes plans each once (the submitter's
+            // per-image host time bounds small-image streams)
+            std::vector<hj::Tile> &tiles = tiles_buf;
+            std::vector<Plan::Group> &groups = groups_buf;
             if (vs == HJ_OK) {
-                build_tiles(&im, 1, tiles, groups);
+                const PlanKey key{im.width, im.height, im.subsampling, im.flags, im.row0, im.n_rows};
+                auto it = plan_cache.find(key);
+                if (it == plan_cache.end()) {
+                    tiles.clear();
+                    groups.clear();
+                    build_tiles(&im, 1, tiles, groups);
+                    if (plan_cache.size() < 4096) plan_cache.emplace(key, std::make_pair(tiles, groups));
+                } else {
+                    tiles = it->second.first;
+                    groups = it->second.second;
+                }
                 if (1024 + 256 + sizeof(hj::Tile) * tiles.size() > plan_bytes) vs = fail(HJ_ERR_ARG, "stream: tile plan too large");
             }
             if (vs != HJ_OK) {
@@ -1212,11 +1238,17 @@ extern "C" hj_status hj_stream_run(const hj_stream_image_t *images, int32_t n, i
             size_t coef_b = 0;
             cudaError_t e = cudaSuccess;
             const int64_t plane_off[3] = {0, ny * 64, (ny + nc) * 64}, per_row[3] = {ypr, cpr, cpr};
-            for (int pl = 0; pl < 3 && e == cudaSuccess; ++pl) {
-                const int64_t first = plane_off[pl] + (int64_t)lo * per_row[pl] * 64;
-                const size_t bytes = (size_t)(hi - lo) * per_row[pl] * 128;
-                e = cudaMemcpyAsync(dy + first, sl.h_coef + first, bytes, cudaMemcpyHostToDevice, sl.stream);
-                coef_b += bytes;
+            if (lo == 0 && hi == im.mcu_rows) {
+                // whole image: the three planes are contiguous in the slot - one copy
+                coef_b = (size_t)(ny + 2 * nc) * 128;
+                e = cudaMemcpyAsync(dy, sl.h_coef, coef_b, cudaMemcpyHostToDevice, sl.stream);
+            } else {
+                for (int pl = 0; pl < 3 && e == cudaSuccess; ++pl) {
+                    const int64_t first = plane_off[pl] + (int64_t)lo * per_row[pl] * 64;
+                    const size_t bytes = (size_t)(hi - lo) * per_row[pl] * 128;
+                    e = cudaMemcpyAsync(dy + first, sl.h_coef + first, bytes, cudaMemcpyHostToDevice, sl.stream);
+                    coef_b += bytes;
+                }
             }
             if (e == cudaSuccess) e = cudaMemcpyAsync(misc, sl.h_plan, plan_b, cudaMemcpyHostToDevice, sl.stream);
             for (const auto &gr : groups) {
