@@ -373,17 +373,24 @@ __device__ __forceinline__ bool screen_cols(const int16_t *__restrict__ src, con
     return (acc >> 15) == 0;
 }
 
-// 4:4:4 / 4:2:2 take screen_cols (measured +4 % / +1 %); 4:2:0, whose kernel
-// sits at the 128-register cap with more live state, spills more with it
-// and keeps screen_rows (-8 % otherwise).
+// 4:4:4 takes screen_cols (measured +4 %).  4:2:0 and 4:2:2 keep
+// screen_rows: the 4:2:0 kernel sits at the 128-register cap with more live
+// state and spills with screen_cols (-8 %); 4:2:2 with screen_rows fits 128
+// registers without spills and runs 8 CTAs (16 warps) per SM instead of
+// 6 x 150 registers with screen_cols (+4.8 %, round 2).
 #ifndef HJ_SCREEN_COLS_420
 #define HJ_SCREEN_COLS_420 0
+#endif
+#ifndef HJ_SCREEN_COLS_422
+#define HJ_SCREEN_COLS_422 0
 #endif
 #ifndef HJ_SCREEN_COLS
 #define HJ_SCREEN_COLS 1
 #endif
 template <int SUB>
-constexpr bool kScreenCols = (SUB != HJ_SUB_420 && HJ_SCREEN_COLS) || HJ_SCREEN_COLS_420;
+constexpr bool kScreenCols = SUB == HJ_SUB_444   ? HJ_SCREEN_COLS != 0
+                             : SUB == HJ_SUB_422 ? HJ_SCREEN_COLS_422 != 0
+                                                 : HJ_SCREEN_COLS_420 != 0;
 template <int SUB>
 __device__ __forceinline__ bool screen_block(const int16_t *__restrict__ src, const float *qf, uint32_t (&out)[16]) {
     if constexpr (kScreenCols<SUB>) return screen_cols(src, qf, out);

@@ -23,9 +23,9 @@ static_assert(sizeof(Tile) == 32, "Tile layout");
 // CTA size and residency: small CTAs sweep their strips independently, so
 // barrier waits stay local to a strip.  4:2:0 uses 4-warp CTAs (its wider
 // per-step pixel work balances the float64 fallback better), 4:4:4 / 4:2:2
-// 2-warp CTAs.  CTAs per SM (launch bounds): 4:4:4 runs 8 CTAs and 4:2:0 4
-// CTAs (16 warps, 128 registers; 4:2:x chroma is stored as 2-byte pairs to
-// fit), 4:2:2 6 CTAs (12 warps, 168 registers: it was slower at 16).
+// 2-warp CTAs.  CTAs per SM (launch bounds): 4:4:4 and 4:2:2 run 8 CTAs and
+// 4:2:0 4 CTAs (16 warps, 128 registers; 4:2:x chroma is stored as 2-byte
+// pairs to fit; 4:2:2 with the row-pair screen, hj_render.cu kScreenCols).
 // Measured: tools/experiments/README.md.
 #ifndef HJ_THREADS_420
 #define HJ_THREADS_420 128
@@ -43,7 +43,7 @@ constexpr int threads_for(int sub) {
 #define HJ_CTAS_444 8
 #endif
 #ifndef HJ_CTAS_422
-#define HJ_CTAS_422 6
+#define HJ_CTAS_422 8
 #endif
 #ifndef HJ_CTAS_420
 #define HJ_CTAS_420 4
