@@ -68,7 +68,7 @@ def parse_args():
     ap.add_argument("--e2e-chunk", type=int, default=4, help="images per pipelined H2D/render/D2H chunk")
     ap.add_argument("--e2e-threads", type=int, default=0,
                     help="host threads calling the render_rows plugin (the reference's lanes call it from a "
-                         "pool); 0 = min(8, this rank's share of the host cores)")
+                         "pool); 0 = min(12, this rank's share of the host cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-variants", action="store_true",
                     help="4:4:4/4:2:2: time the shipped/patched/fallback reference builds, 1 and N processes")
@@ -883,7 +883,7 @@ def main():
         c = coeffs[i]
         fn(c.y_blocks, c.cb_blocks, c.cr_blocks, qts[i], out_arrays[i], w, h, mpr, row0, n_rows, idct_arg(args))
 
-    n_thr = args.e2e_threads or max(1, min(8, len(os.sched_getaffinity(0)) // world))
+    n_thr = args.e2e_threads or max(1, min(12, len(os.sched_getaffinity(0)) // world))
     from paper_1311_5304_b200 import _lib as hjlib
     with ThreadPoolExecutor(n_thr) as ex:
         for _ in range(2):
