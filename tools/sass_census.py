@@ -12,7 +12,7 @@ funcs = re.split(r"\n\s+Function : ", out)
 print(f"# cuobjdump -sass {LIB}: static instruction counts per render kernel")
 for f in funcs[1:]:
     name = f.split("\n", 1)[0].strip()
-    if "render_kernel" not in name:
+    if "render_kernel" not in name and "render_tc_kernel" not in name and "unpack_blocks" not in name:
         continue
     ops = collections.Counter()
     for line in f.splitlines():
@@ -23,9 +23,13 @@ for f in funcs[1:]:
     for k, v in ops.items():
         base[k.split(".")[0]] += v
     sub = re.search(r"render_kernelILi(\d)ELi(\d)E", name)
-    label = f"render_kernel<{sub.group(1)},{sub.group(2)}>" if sub else name
+    tcs = re.search(r"render_tc_kernelILi(\d)E", name)
+    label = (f"render_kernel<{sub.group(1)},{sub.group(2)}>" if sub else
+             f"render_tc_kernel<{tcs.group(1)}>" if tcs else
+             "unpack_blocks_kernel" if "unpack_blocks" in name else name)
     print(f"\n## {label}  ({sum(ops.values())} instructions)")
     print("  top opcodes: " + ", ".join(f"{k} {v}" for k, v in base.most_common(24)))
     special = {k: v for k, v in ops.items() if k.split(".")[0] in
-               ("FADD2", "FFMA2", "FMUL2", "I2IP", "UBLKPF", "LDG") or k.startswith("LDG.E.NA") or "256" in k}
+               ("FADD2", "FFMA2", "FMUL2", "I2IP", "UBLKPF", "LDG", "LDTM", "UTCBAR", "SYNCS")
+               or k.startswith("UTC") or k.startswith("LDG.E.NA") or "256" in k}
     print("  Blackwell / path markers: " + ", ".join(f"{k} {v}" for k, v in sorted(special.items())))
