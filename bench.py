@@ -888,16 +888,23 @@ def main():
     with ThreadPoolExecutor(n_thr) as ex:
         for _ in range(2):
             list(ex.map(one, range(batch)))
-        barrier(pg)
-        h2d0 = hjlib.lib.hj_h2d_bytes()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            list(ex.map(one, range(batch)))
-        e2e_s = allreduce_max(pg, time.perf_counter() - t0)
-        # bytes the plugin really moved host->device (packed coefficients when
-        # the packed transfer is on), per step
-        plugin_h2d = (hjlib.lib.hj_h2d_bytes() - h2d0) // e2e_steps
+        # three timed runs of e2e_steps steps, the median reported: the PCIe
+        # link and the host cores are shared with the box, single runs vary
+        e2e_runs, h2d_runs = [], []
+        for _ in range(3):
+            barrier(pg)
+            h2d0 = hjlib.lib.hj_h2d_bytes()
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                list(ex.map(one, range(batch)))
+            e2e_runs.append(allreduce_max(pg, time.perf_counter() - t0))
+            # bytes the plugin really moved host->device (packed coefficients
+            # when the packed transfer is on), per step
+            h2d_runs.append((hjlib.lib.hj_h2d_bytes() - h2d0) // e2e_steps)
+        e2e_s = sorted(e2e_runs)[1]
+        plugin_h2d = h2d_runs[e2e_runs.index(e2e_s)]
     e2e_value = px_all * e2e_steps / e2e_s / 1e6
+    e2e_run_values = [round(px_all * e2e_steps / t / 1e6, 1) for t in e2e_runs]
     e2e_lane_value = px_all * e2e_steps / e2e_lane_s / 1e6
     # the e2e output must be the kernel's output: spot-check one image against the oracle
     _, _, c0, q0 = images[0]
@@ -948,7 +955,8 @@ def main():
                     "h2d_bytes_per_step": int(plugin_h2d), "d2h_bytes_per_step": io["d2h_bytes"],
                     "dense_h2d_bytes_per_step": io["h2d_bytes"],
                     "packed_h2d": bool(hjlib.lib.hj_packed_h2d_active()),
-                    "steps": e2e_steps, "bit_exact_vs_oracle": exact,
+                    "steps": e2e_steps, "runs": e2e_run_values, "reported": "median of the 3 runs",
+                    "bit_exact_vs_oracle": exact,
                     "api": f"kernels.cuda.render_rows_{sub} (reference backend contract) per image from "
                            f"{n_thr} host threads, pinned host buffers"
                            + (", coefficients packed on the host (nonzero masks + int8/int16 values) "
