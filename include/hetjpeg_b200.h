@@ -132,12 +132,19 @@ uint64_t hj_tc_launch_count(void);
  * coefficients (int8 when all fit), copies that, and expands it on the device -
  * lossless; the copy is PCIe-bound and 1080p q90 blocks shrink from 128 to
  * ~47 B.  Default (mode -1): packed when the host CPU has AVX-512 VBMI2, >= 4
- * calls are in flight (a saturated link), the call has <= 64k blocks and its
- * first 4096 Y blocks pack below 0.45 of their dense bytes; otherwise dense.
+ * calls are in flight (a saturated link) and the call's first 4096 Y blocks
+ * pack below 0.45 of their dense bytes; otherwise dense.  Calls above 64k
+ * blocks are packed in bands (hj_set_pack_band).
  * Mode 0 forces the dense copy, 1 forces packing; HJ_PACK_H2D=0/1 in the
  * environment does the same.  hj_packed_h2d_active: 0 off, 1 forced, 2 auto. */
 hj_status hj_set_packed_h2d(int32_t mode);
 int32_t hj_packed_h2d_active(void);
+/* Packed calls above 64k blocks (default) are sent in bands of MCU rows of
+ * ~32k blocks: band k+1 packs on the host while band k copies and band k-1
+ * renders and returns its RGB rows.  hj_set_pack_band(n > 0) sets both the
+ * threshold and the band size to n blocks (tests; HJ_PACK_BAND=n in the
+ * environment does the same); 0 restores the default. */
+hj_status hj_set_pack_band(int64_t blocks);
 /* Bytes the synchronous drop-in copied host->device so far (packed or dense). */
 uint64_t hj_h2d_bytes(void);
 /* The packer / a host unpacker (tests): returns the value bytes written. `vals`

@@ -156,6 +156,7 @@ _SIG = {
     "hj_tc_launch_count": (C.c_uint64, []),
     "hj_set_packed_h2d": (C.c_int, [C.c_int32]),
     "hj_packed_h2d_active": (C.c_int32, []),
+    "hj_set_pack_band": (C.c_int, [C.c_int64]),
     "hj_h2d_bytes": (C.c_uint64, []),
     "hj_pack_blocks": (C.c_int64, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "hj_unpack_blocks_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),

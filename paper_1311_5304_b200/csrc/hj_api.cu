@@ -331,6 +331,15 @@ struct SyncCtx {
     void *dpack = nullptr;           // their device copy
     size_t dpack_bytes = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // banded packed transfer (large calls): two host / device staging slots,
+    // an event per slot marking its copy done
+    void *hring[2] = {nullptr, nullptr};
+    size_t hring_bytes[2] = {0, 0};
+    void *dring[2] = {nullptr, nullptr};
+    size_t dring_bytes[2] = {0, 0};
+    cudaEvent_t ring_ev[2] = {nullptr, nullptr};
+    cudaEvent_t band_ev[2] = {nullptr, nullptr};  // a band's blocks expanded on `up`
+    cudaStream_t up = nullptr;                      // the bands' copies + expansion
     void release() {
         if (device >= 0) {
             cudaFree(coef);
@@ -338,6 +347,13 @@ struct SyncCtx {
             cudaFree(misc);
             cudaFree(dpack);
             if (hpack) cudaFreeHost(hpack);
+            for (int k = 0; k < 2; ++k) {
+                if (hring[k]) cudaFreeHost(hring[k]);
+                cudaFree(dring[k]);
+                if (ring_ev[k]) cudaEventDestroy(ring_ev[k]);
+                if (band_ev[k]) cudaEventDestroy(band_ev[k]);
+            }
+            if (up) cudaStreamDestroy(up);
             for (auto &e : ev)
                 if (e) cudaEventDestroy(e);
             if (stream) cudaStreamDestroy(stream);
@@ -383,6 +399,11 @@ constexpr double kPackMaxRatio = 0.45;   // pack only below this fraction of the
 // copy alone runs at ~50 GB/s, and a multi-MB pinned staging buffer per
 // calling thread is not worth it (measured: 24 MP 4:2:0 images 13.4k -> 2.0k)
 constexpr int64_t kPackMaxBlocks = 1 << 16;  // 8 MB of dense coefficients
+// ... unless they are packed in bands of MCU rows (render_rows_banded): band
+// k+1 is packed on the host while band k copies and band k-1 renders and
+// copies its RGB back, so the packing hides behind the link.
+constexpr int64_t kPackBandBlocks = 1 << 15;
+std::atomic<int64_t> g_pack_band{0};  // hj_set_pack_band: 0 default, else band size and threshold
 std::atomic<int> g_inflight{0};
 int pack_env() {
     static const int env = [] {
@@ -410,10 +431,19 @@ hj_status ctx_get(SyncCtx **out) {
             c.coef = c.rgb = c.misc = c.dpack = c.hpack = nullptr;
             c.coef_bytes = c.rgb_bytes = c.misc_bytes = c.dpack_bytes = c.hpack_bytes = 0;
             for (auto &e : c.ev) e = nullptr;
+            for (int k = 0; k < 2; ++k) {
+                c.hring[k] = c.dring[k] = nullptr;
+                c.hring_bytes[k] = c.dring_bytes[k] = 0;
+                c.ring_ev[k] = c.band_ev[k] = nullptr;
+            }
+            c.up = nullptr;
             c.stream = nullptr;
         }
         HJ_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         for (auto &e : c.ev) HJ_CUDA(cudaEventCreate(&e));
+        for (auto &e : c.ring_ev) HJ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto &e : c.band_ev) HJ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        HJ_CUDA(cudaStreamCreateWithFlags(&c.up, cudaStreamNonBlocking));
         c.device = dev;
     }
     *out = &c;
@@ -684,6 +714,11 @@ hj_status hj_set_packed_h2d(int32_t mode) {
     g_pack_mode.store(mode);
     return HJ_OK;
 }
+hj_status hj_set_pack_band(int64_t blocks) {
+    if (blocks < 0) return fail(HJ_ERR_ARG, "pack band must be >= 0 blocks");
+    g_pack_band.store(blocks);
+    return HJ_OK;
+}
 int32_t hj_packed_h2d_active(void) {
     const int m = g_pack_mode.load(std::memory_order_relaxed);
     if (m >= 0) return m;
@@ -703,6 +738,135 @@ hj_status hj_unpack_blocks_host(const uint64_t *mask, const uint32_t *off, const
     if (n < 0 || (n > 0 && (!mask || !off || !dc || !vals || !dst)))
         return fail(HJ_ERR_ARG, "hj_unpack_blocks_host: bad arguments");
     hj::unpack_blocks_host(mask, off, dc, vals, n, dst);
+    return HJ_OK;
+}
+
+// Banded transfer of one large drop-in call: the call's MCU rows in bands of
+// ~band_blocks blocks, each sent dense or packed (policy: 0 dense, 1 packed,
+// 2 packed while >= kPackMinCallers calls are in flight).  Band j's three records (Y, Cb, Cr; the
+// hj_pack.h format) are packed into host slot j%2 while stream `up` copies
+// and expands band j-1 and the call's stream renders band j-2 and returns
+// its RGB rows (copies in both directions at once).  A band is rendered one
+// band late, so a 4:2:0 band's chroma context row (the next band's first)
+// is on the device.  Same bytes as the dense path.
+static hj_status render_rows_banded(SyncCtx *c, const hj_image_t &im_all, const int32_t *q3x64,
+                                    const int16_t *hy, const int16_t *hcb, const int16_t *hcr, int16_t *dy,
+                                    int16_t *dcb, int16_t *dcr, int c_lo, int c_hi, int64_t per_row_y,
+                                    int64_t per_row_c, int mh, int py0, uint8_t *rgb, int64_t band_blocks,
+                                    int policy) {
+    const int row0 = im_all.row0, n_rows = im_all.n_rows, width = im_all.width, height = im_all.height;
+    const int rpb = (int)std::max<int64_t>(1, band_blocks / (per_row_y + 2 * per_row_c));
+    const int nb = (n_rows + rpb - 1) / rpb;
+    auto yrow = [&](int j) { return j >= nb ? row0 + n_rows : row0 + j * rpb; };  // band j: MCU rows [yrow(j), yrow(j+1))
+    auto crow = [&](int j) { return j == 0 ? c_lo : j >= nb ? c_hi : yrow(j); };  // its chroma rows
+    // plan: [q 768 B][one image desc per band][every band's tiles][8 zero bytes: the record table]
+    const size_t img_off = 1024;
+    const size_t tile_off = (img_off + sizeof(hj_image_t) * (size_t)nb + 15) & ~(size_t)15;
+    std::vector<hj_image_t> ims((size_t)nb, im_all);
+    std::vector<hj::Tile> tiles;
+    std::vector<std::vector<Plan::Group>> groups((size_t)nb);
+    for (int j = 0; j < nb; ++j) {
+        ims[j].row0 = yrow(j);
+        ims[j].n_rows = yrow(j + 1) - yrow(j);
+        build_tiles(&ims[j], 1, tiles, groups[j]);  // tile.image 0 = this band's descriptor
+    }
+    const size_t tab_off = (tile_off + sizeof(hj::Tile) * tiles.size() + 15) & ~(size_t)15;
+    const size_t plan_bytes = tab_off + 8;
+    hj_status st = ensure(&c->misc, &c->misc_bytes, plan_bytes);
+    if (st != HJ_OK) return st;
+    uint8_t *misc = static_cast<uint8_t *>(c->misc);
+    for (auto &m : ims) m.q = reinterpret_cast<const int32_t *>(misc);
+    c->host_plan.assign(plan_bytes, 0);
+    std::memcpy(c->host_plan.data(), q3x64, 768);
+    std::memcpy(c->host_plan.data() + img_off, ims.data(), sizeof(hj_image_t) * (size_t)nb);
+    if (!tiles.empty()) std::memcpy(c->host_plan.data() + tile_off, tiles.data(), sizeof(hj::Tile) * tiles.size());
+    // staging slots sized for the largest band, before any copy of this call
+    auto rec_hdr = [](int64_t n) { return ((size_t)n * 14 + 15) & ~(size_t)15; };
+    auto rec_bound = [&](int64_t n) { return rec_hdr(n) + ((hj::pack_vals_bound(n) + 15) & ~(size_t)15); };
+    size_t need = 16;
+    for (int j = 0; j < nb; ++j)
+        need = std::max(need, rec_bound((int64_t)(yrow(j + 1) - yrow(j)) * per_row_y) +
+                                  2 * rec_bound((int64_t)(crow(j + 1) - crow(j)) * per_row_c));
+    for (int k = 0; k < 2; ++k) {
+        st = ensure_host(&c->hring[k], &c->hring_bytes[k], need);
+        if (st == HJ_OK) st = ensure(&c->dring[k], &c->dring_bytes[k], need);
+        if (st != HJ_OK) return st;
+    }
+    HJ_CUDA(cudaMemcpyAsync(misc, c->host_plan.data(), plan_bytes, cudaMemcpyHostToDevice, c->up));
+    g_h2d_bytes.fetch_add(plan_bytes, std::memory_order_relaxed);
+    const hj_image_t *dimg = reinterpret_cast<const hj_image_t *>(misc + img_off);
+    const hj::Tile *dtiles = reinterpret_cast<const hj::Tile *>(misc + tile_off);
+    const uint64_t *dtab = reinterpret_cast<const uint64_t *>(misc + tab_off);
+    auto render_band = [&](int j) -> hj_status {
+        for (const auto &g : groups[j]) {
+            cudaError_t e = hj::launch_render(g.sub, hj::mode_of_kind(g.kind), dimg + j, dtiles + g.offset, g.count,
+                                              c->stream);
+            if (e != cudaSuccess) return cuda_fail(e, "render kernel launch");
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+        }
+        const int y0 = yrow(j) * mh, y1 = std::min(height, yrow(j + 1) * mh);
+        if (y1 > y0)
+            HJ_CUDA(cudaMemcpyAsync(rgb + (size_t)y0 * width * 3,
+                                    static_cast<uint8_t *>(c->rgb) + (size_t)(y0 - py0) * width * 3,
+                                    (size_t)(y1 - y0) * width * 3, cudaMemcpyDeviceToHost, c->stream));
+        return HJ_OK;
+    };
+    for (int j = 0; j < nb; ++j) {
+        const int slot = j & 1;
+        if (j >= 2) HJ_CUDA(cudaEventSynchronize(c->ring_ev[slot]));  // band j-2's copy has left the slot
+        uint8_t *hp = static_cast<uint8_t *>(c->hring[slot]);
+        uint8_t *dp = static_cast<uint8_t *>(c->dring[slot]);
+        const int64_t ny = (int64_t)(yrow(j + 1) - yrow(j)) * per_row_y;
+        const int64_t nc = (int64_t)(crow(j + 1) - crow(j)) * per_row_c;
+        const int64_t yb = (int64_t)(yrow(j) - row0) * per_row_y * 64, cbo = (int64_t)(crow(j) - c_lo) * per_row_c * 64;
+        const int16_t *src[3] = {hy + yb, hcb + cbo, hcr + cbo};
+        int16_t *dst[3] = {dy + yb, dcb + cbo, dcr + cbo};
+        const int64_t cnt[3] = {ny, nc, nc};
+        const bool pk = policy == 1 || (policy == 2 && g_inflight.load(std::memory_order_relaxed) >= kPackMinCallers);
+        if (!pk) {
+            // dense band: straight into the block planes
+            for (int p = 0; p < 3; ++p)
+                if (cnt[p] > 0) HJ_CUDA(cudaMemcpyAsync(dst[p], src[p], (size_t)cnt[p] * 128, cudaMemcpyHostToDevice, c->up));
+            g_h2d_bytes.fetch_add((size_t)(ny + 2 * nc) * 128, std::memory_order_relaxed);
+            HJ_CUDA(cudaEventRecord(c->ring_ev[slot], c->up));
+            HJ_CUDA(cudaEventRecord(c->band_ev[slot], c->up));
+            HJ_CUDA(cudaStreamWaitEvent(c->stream, c->band_ev[slot], 0));
+            if (j >= 1) {
+                st = render_band(j - 1);
+                if (st != HJ_OK) return st;
+            }
+            continue;
+        }
+        size_t roff[3], total = 0;
+        for (int p = 0; p < 3; ++p) {
+            const int64_t n = cnt[p];
+            uint8_t *r = hp + total;
+            const size_t vb = n > 0 ? hj::pack_blocks(src[p], n, reinterpret_cast<uint64_t *>(r),
+                                                      reinterpret_cast<uint32_t *>(r + n * 8),
+                                                      reinterpret_cast<int16_t *>(r + n * 12), r + rec_hdr(n), 0)
+                                    : 0;
+            roff[p] = total;
+            total += (rec_hdr(n) + vb + 15) & ~(size_t)15;
+        }
+        HJ_CUDA(cudaMemcpyAsync(dp, hp, total, cudaMemcpyHostToDevice, c->up));
+        HJ_CUDA(cudaEventRecord(c->ring_ev[slot], c->up));
+        g_h2d_bytes.fetch_add(total, std::memory_order_relaxed);
+        for (int p = 0; p < 3; ++p) {
+            if (cnt[p] <= 0) continue;
+            cudaError_t e = hj::launch_unpack_blocks(dp + roff[p], dtab, cnt[p], rec_hdr(cnt[p]), cnt[p], dst[p], c->up);
+            if (e != cudaSuccess) return cuda_fail(e, "unpack kernel launch");
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+        }
+        HJ_CUDA(cudaEventRecord(c->band_ev[slot], c->up));
+        HJ_CUDA(cudaStreamWaitEvent(c->stream, c->band_ev[slot], 0));  // band j on the device
+        if (j >= 1) {
+            st = render_band(j - 1);
+            if (st != HJ_OK) return st;
+        }
+    }
+    st = render_band(nb - 1);
+    if (st != HJ_OK) return st;
+    HJ_CUDA(cudaStreamSynchronize(c->stream));
     return HJ_OK;
 }
 
@@ -786,8 +950,19 @@ static hj_status render_rows_impl(const int16_t *y, const int16_t *cb, const int
         ~Leave() { g_inflight.fetch_sub(1, std::memory_order_relaxed); }
     } leave;
     const bool forced = g_pack_mode.load(std::memory_order_relaxed) == 1 || pack_env() == 1;
-    bool pack = pack_h2d_on(inflight) && nblk > 0 && hj::pack_vals_bound(nblk) < 0x7fffffffull &&
-                (forced || nblk <= kPackMaxBlocks);
+    static const int64_t band_env = [] {
+        const char *v = std::getenv("HJ_PACK_BAND");
+        return v && v[0] ? std::max<int64_t>(0, std::atoll(v)) : (int64_t)0;
+    }();
+    const int64_t band_set = g_pack_band.load(std::memory_order_relaxed);
+    const int64_t band_cfg = band_set > 0 ? band_set : band_env;
+    const int64_t single_max = band_cfg > 0 ? band_cfg : kPackMaxBlocks;
+    // large packed calls (outside the timed variant, which keeps one copy
+    // per phase) go in bands of MCU rows, each band packed or dense
+    const bool banded = !phase_ms && nblk > single_max;
+    bool pack = nblk > 0 && (banded ? (forced || pack_h2d_on(kPackMinCallers))
+                                    : pack_h2d_on(inflight) && hj::pack_vals_bound(nblk) < 0x7fffffffull &&
+                                          (forced || nblk <= kPackMaxBlocks));
     const size_t rec_hdr = ((size_t)nblk * 14 + 15) & ~(size_t)15;
     const size_t tab_off = (misc_need + 15) & ~(size_t)15;  // record offset table, after the plan
     size_t rec_bytes = 0;
@@ -805,6 +980,11 @@ static hj_status render_rows_impl(const int16_t *y, const int16_t *cb, const int
                                           reinterpret_cast<int16_t *>(sp + np * 12), sp + np * 14, 0);
         if ((double)(14 * np + vb) > kPackMaxRatio * 128.0 * (double)np) pack = false;
     }
+    // (a large call the probe sends dense stays one copy each way: dense
+    // bands measured slower, tools/experiments/README.md)
+    if (banded && pack)  // policy: 1 every band packed, 2 packed while >= kPackMinCallers calls are in flight
+        return render_rows_banded(c, im, q3x64, hy, hcb, hcr, dy, dcb, dcr, c_lo, c_hi, per_row_y, per_row_c, mh,
+                                  py0, rgb, band_cfg > 0 ? band_cfg : kPackBandBlocks, forced ? 1 : 2);
     if (pack) {
         st = ensure_host(&c->hpack, &c->hpack_bytes, rec_hdr + hj::pack_vals_bound(nblk));
         if (st != HJ_OK) return st;
