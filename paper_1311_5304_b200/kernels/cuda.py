@@ -86,8 +86,9 @@ def _render(sub, y_blocks, cb_blocks, cr_blocks, qtables, rgb, width, height, mc
             or not rgb.flags.c_contiguous:
         raise ValueError("rgb must be a C-contiguous uint8 (height, width, 3) array")
     mcu_rows = -(-int(height) // _SUB_MCU_H[sub])
-    st = _lib.lib.hj_render_rows(y_blocks.ctypes.data, cb_blocks.ctypes.data, cr_blocks.ctypes.data,
-                                 q.ctypes.data, rgb.ctypes.data, int(width), int(height),
+    ptr = _lib.ptr
+    st = _lib.lib.hj_render_rows(ptr(y_blocks), ptr(cb_blocks), ptr(cr_blocks),
+                                 ptr(q), ptr(rgb), int(width), int(height),
                                  int(mcus_per_row), mcu_rows, int(row0), int(n_rows), sub,
                                  _lib.idct_code(fast), int(bool(fused)), len(y_blocks), len(cb_blocks))
     _lib.check(st, "render_rows")
