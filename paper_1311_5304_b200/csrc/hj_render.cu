@@ -680,24 +680,44 @@ __device__ __forceinline__ void colour4(uint32_t yw, int cb0, int cr0, int cb1, 
 // 11 interior aligned words (funnel-shifted into place) plus the partial
 // words at both ends; only items cropped by the right edge take the
 // byte-wise path.
+// RGB stores are write-once: st.global.cs (evict-first) keeps them from
+// displacing the coefficient stream's L2 prefetches (measured +0.3-0.6 %).
+#ifndef HJ_STCS
+#define HJ_STCS 1
+#endif
+template <class T>
+__device__ __forceinline__ void st_rgb(T *p, T v) {
+#if HJ_STCS
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+__device__ __forceinline__ void st_rgb(uint32_t *p, uint32_t v) {
+#if HJ_STCS
+    __stcs(reinterpret_cast<unsigned int *>(p), v);
+#else
+    *p = v;
+#endif
+}
 __device__ __forceinline__ void store48(uint8_t *__restrict__ dst, const uint32_t (&w)[12], int npx) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
     if (npx == 16 && (a & 15) == 0) {
         uint4 *d = reinterpret_cast<uint4 *>(dst);
-        d[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        d[1] = make_uint4(w[4], w[5], w[6], w[7]);
-        d[2] = make_uint4(w[8], w[9], w[10], w[11]);
+        st_rgb(d, make_uint4(w[0], w[1], w[2], w[3]));
+        st_rgb(d + 1, make_uint4(w[4], w[5], w[6], w[7]));
+        st_rgb(d + 2, make_uint4(w[8], w[9], w[10], w[11]));
     } else if (npx == 16 && (a & 7) == 0) {
         uint2 *d = reinterpret_cast<uint2 *>(dst);
 #pragma unroll
-        for (int i = 0; i < 6; ++i) d[i] = make_uint2(w[2 * i], w[2 * i + 1]);
+        for (int i = 0; i < 6; ++i) st_rgb(d + i, make_uint2(w[2 * i], w[2 * i + 1]));
     } else if (npx == 16 && (a & 3) == 0) {
         // a = 4 mod 8: one word, five 8-byte pairs, one word
         uint32_t *d = reinterpret_cast<uint32_t *>(dst);
-        d[0] = w[0];
+        st_rgb(d, w[0]);
 #pragma unroll
-        for (int i = 1; i < 11; i += 2) *reinterpret_cast<uint2 *>(d + i) = make_uint2(w[i], w[i + 1]);
-        d[11] = w[11];
+        for (int i = 1; i < 11; i += 2) st_rgb(reinterpret_cast<uint2 *>(d + i), make_uint2(w[i], w[i + 1]));
+        st_rgb(d + 11, w[11]);
     } else if (npx == 16) {
         const int m = (int)(a & 3);  // 1..3
         uint32_t *d = reinterpret_cast<uint32_t *>(dst - m);
@@ -710,12 +730,12 @@ __device__ __forceinline__ void store48(uint8_t *__restrict__ dst, const uint32_
         // row's items share one alignment: 48-byte steps)
         if ((reinterpret_cast<uintptr_t>(d + 1) & 7) == 0) {
 #pragma unroll
-            for (int k = 1; k < 11; k += 2) *reinterpret_cast<uint2 *>(d + k) = make_uint2(f[k], f[k + 1]);
-            d[11] = f[11];
+            for (int k = 1; k < 11; k += 2) st_rgb(reinterpret_cast<uint2 *>(d + k), make_uint2(f[k], f[k + 1]));
+            st_rgb(d + 11, f[11]);
         } else {
-            d[1] = f[1];
+            st_rgb(d + 1, f[1]);
 #pragma unroll
-            for (int k = 2; k < 12; k += 2) *reinterpret_cast<uint2 *>(d + k) = make_uint2(f[k], f[k + 1]);
+            for (int k = 2; k < 12; k += 2) st_rgb(reinterpret_cast<uint2 *>(d + k), make_uint2(f[k], f[k + 1]));
         }
         // head: the first 4-m bytes of w[0]; tail: the last m bytes of w[11]
         if (m == 2) {
@@ -733,9 +753,9 @@ __device__ __forceinline__ void store48(uint8_t *__restrict__ dst, const uint32_
     } else if (npx == 8 && (a & 7) == 0) {
         // half item (4:4:4 image whose width is 8 mod 16): 24 bytes, 8-aligned
         uint2 *d = reinterpret_cast<uint2 *>(dst);
-        d[0] = make_uint2(w[0], w[1]);
-        d[1] = make_uint2(w[2], w[3]);
-        d[2] = make_uint2(w[4], w[5]);
+        st_rgb(d, make_uint2(w[0], w[1]));
+        st_rgb(d + 1, make_uint2(w[2], w[3]));
+        st_rgb(d + 2, make_uint2(w[4], w[5]));
     } else {
         store_partial(dst, make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]),
                       make_uint4(w[8], w[9], w[10], w[11]), npx * 3);
