@@ -649,6 +649,33 @@ __device__ __forceinline__ int grab32(int *taken) {
     return __shfl_sync(0xffffffffu, base, 0) + (threadIdx.x & 31);
 }
 
+// HJ_EARLY_A (measured and rejected, default 0; tools/experiments/README.md):
+// no barrier at the end of a step; a thread starts the next step's phase A
+// (coefficient loads + first screen: registers only) as soon as its own
+// phase B is done, and waits on barrier 1 (non-aligned: reached from
+// different code points) before its first shared-memory write.
+#ifndef HJ_EARLY_A
+#define HJ_EARLY_A 0
+#endif
+__device__ __forceinline__ void hj_barrier_early() { asm volatile("barrier.sync 1;" ::: "memory"); }
+
+// Reference mode: each warp's first round of a step is its own 32 items (the
+// counter starts at blockDim.x), so only the later rounds take the atomic
+// (+0.5 % at 1080p 4:2:0).  The islow kernel keeps the atomic-only queue
+// (-1 % with the static round).
+#ifndef HJ_GRAB_STATIC
+#define HJ_GRAB_STATIC 1
+#endif
+template <int MODE>
+__device__ __forceinline__ constexpr bool grab_static() { return HJ_GRAB_STATIC && MODE == kModeRef; }
+template <int MODE>
+__device__ __forceinline__ int grab_base() { return grab_static<MODE>() ? (int)blockDim.x : 0; }
+template <int MODE>
+__device__ __forceinline__ int grab_first(int *taken) {
+    if constexpr (grab_static<MODE>()) return (int)threadIdx.x;
+    else return grab32(taken);
+}
+
 // Colour + pack of 4 pixels (Y bytes of `yw`, chroma ints) -> 12 RGB bytes
 // in 3 words.  Small live ranges on purpose: the colour constants stay in
 // registers instead of being rematerialised per pixel.
@@ -952,7 +979,7 @@ __device__ __forceinline__ void pixel_phase(SM &sm, const hj_image_t &im, const 
             // jobs overwrote its slot, else still in the slot
             const uint16_t *cprev = do_c ? &sm.cs[24][0] : &sm.cs[0][0] + (((R + 2) % 3) * 8 + 7) * G::CW;
 #pragma unroll 1
-            for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
+            for (int i0 = grab_first<MODE>(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
                 const int i = i0;
                 if (i >= n_items) continue;
                 // row-major items: adjacent lanes store adjacent 48-byte runs
@@ -1007,7 +1034,7 @@ __device__ __forceinline__ void pixel_phase(SM &sm, const hj_image_t &im, const 
             const float inv_w = 1.0f / (float)gw;
             const uint16_t *crow0 = &sm.cs[0][0] + (par ^ 1) * 8 * G::CW;
 #pragma unroll 1
-            for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
+            for (int i0 = grab_first<MODE>(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
                 const int i = i0;
                 if (i >= n_items) continue;
                 const int y = __float2int_rd(((float)i + 0.5f) * inv_w), g = i - y * gw;
@@ -1038,7 +1065,7 @@ __device__ __forceinline__ void pixel_phase(SM &sm, const hj_image_t &im, const 
             const float inv_w = 1.0f / (float)gw;
             const uint8_t *cbp = sm.cbp[par ^ 1], *crp = sm.crp[par ^ 1];
 #pragma unroll 1
-            for (int i0 = grab32(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
+            for (int i0 = grab_first<MODE>(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
                 const int i = i0;
                 if (i >= n_items) continue;
                 const int y = __float2int_rd(((float)i + 0.5f) * inv_w), g = i - y * gw;
@@ -1077,7 +1104,10 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
     if constexpr (!kIslow)
         for (int i = tid; i < 192; i += kThreads)
             sm.qf[i >> 6][qf_slot(kScreenCols<SUB>, (i & 63) >> 3, i & 7)] = (float)((double)im.q[i] * kPre64[i & 63]);
-    if (tid == 0) sm.n_queue[0] = sm.n_queue[1] = sm.n_taken[0] = sm.n_taken[1] = 0;
+    if (tid == 0) {
+        sm.n_queue[0] = sm.n_queue[1] = 0;
+        sm.n_taken[0] = sm.n_taken[1] = grab_base<MODE>();
+    }
 
     const int cm_lo = (SUB == HJ_SUB_444) ? t.m0 : t.m0 - 1;  // first chroma window MCU
     const int n_cm = (SUB == HJ_SUB_444) ? S : S + 2;
@@ -1101,8 +1131,10 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
         const bool do_c = (SUB == HJ_SUB_420) ? (crow >= t.r0 - 1 && crow <= t.r1 && crow >= 0 && crow < mcu_rows)
                                               : do_y;
         if (tid == 0) {
-            sm.n_queue[par ^ 1] = 0;  // last used in step s-1, next in s+1
-            sm.n_taken[par ^ 1] = 0;
+            if (!HJ_EARLY_A) {
+                sm.n_queue[par ^ 1] = 0;  // last used in step s-1, next in s+1
+                sm.n_taken[par ^ 1] = grab_base<MODE>();
+            }
             // bulk L2 prefetch of the next step's coefficient ranges
             const int ny = HJ_PF_L2 ? s + 1 : -1;
             if (ny >= t.r0 && ny < t.r1) {
@@ -1124,6 +1156,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
         {
             const int n_y = do_y ? n_yj : 0;
             const int n_jobs = n_y + (do_c ? n_cm : 0);
+            bool synced = !HJ_EARLY_A;  // passed the deferred end-of-step barrier
 #pragma unroll 1
             for (int j = tid; j < n_jobs; j += kThreads) {
                 const bool is_y = j < n_y;
@@ -1169,7 +1202,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                         cdst = &sm.cs[0][0] + cw0;
                         dA = (2u << 30) | (uint32_t)cw0;
                         dB = (3u << 30) | (uint32_t)cw0;
-                        if constexpr (SUB == HJ_SUB_420) {
+                        if constexpr (SUB == HJ_SUB_420 && !HJ_EARLY_A) {
                             // the slot's old row 7 (MCU row crow-3) is the top
                             // context of MCU row crow-2, drawn this step
                             uint16_t *save = &sm.cs[24][0] + 8 * lm;
@@ -1201,6 +1234,19 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                         ok = true;
                     } else if (!direct) {
                         ok = screen_block<SUB>(k ? srcB : srcA, sm.qf[comp], w);
+                    }
+                    if (!synced) {
+                        // early A: the loads and the first screen of this step
+                        // ran while other warps finished the previous step's
+                        // phase B; shared-memory writes wait for all of them
+                        hj_barrier_early();
+                        synced = true;
+                    }
+                    if constexpr (SUB == HJ_SUB_420 && HJ_EARLY_A) {
+                        if (k == 0 && !is_y) {
+                            uint16_t *save = &sm.cs[24][0] + 8 * lm;
+                            sts128(save, lds128(cdst + 7 * G::CW));
+                        }
                     }
                     if (SUB == HJ_SUB_444 || is_y) {
                         // byte planes: Y (blocks side by side) or Cb / Cr
@@ -1251,14 +1297,21 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
                     }
                 }
             }
+            if (!synced) hj_barrier_early();  // threads without a (drawn) job
         }
         __syncthreads();
+        if (HJ_EARLY_A && tid == 0) {
+            // last used by phase B of step s-1 (done: every thread passed the
+            // early barrier of this step), next by step s+1
+            sm.n_queue[par ^ 1] = 0;
+            sm.n_taken[par ^ 1] = grab_base<MODE>();
+        }
 
         // ---------------- phase B: exact recompute of this step's queue ...
         exact_phase<SUB, MODE, G, kThreads>(sm, smem_raw, im, par, direct);
         // ---------------- ... overlapped with the pixel stage of MCU row s-1
         pixel_phase<SUB, MODE, G>(sm, im, t, s, par, do_c);
-        __syncthreads();
+        if (!HJ_EARLY_A) __syncthreads();
     }
 }
 
@@ -1514,7 +1567,7 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
     const bool direct = (im.flags & HJ_FLAG_DIRECT_IDCT) != 0;
     for (int i = tid; i < 192; i += NT) sm.qi[i >> 6][i & 63] = im.q[i];
     if (tid == 0) {
-        sm.n_queue[0] = sm.n_queue[1] = sm.n_taken[0] = sm.n_taken[1] = 0;
+        sm.n_queue[0] = sm.n_queue[1] = 0; sm.n_taken[0] = sm.n_taken[1] = grab_base<kModeRef>();
         for (int b = 0; b < tcs::kNBuf; ++b) {
             tc::mbar_init(&sm.full[b], 1);
             tc::mbar_init(&sm.empty[b], NT / 32);
@@ -1554,7 +1607,7 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
         const int64_t yblk0 = ((int64_t)s * mpr + t.m0) * YB;  // first Y block of the step
         if (tid == 0) {
             sm.n_queue[par ^ 1] = 0;
-            sm.n_taken[par ^ 1] = 0;
+            sm.n_taken[par ^ 1] = grab_base<kModeRef>();
             const int ny = HJ_PF_L2 ? s + 1 : -1;
             if (ny >= t.r0 && ny < t.r1) {
                 const int64_t b0 = ((int64_t)ny * mpr + t.m0) * YB;
