@@ -186,6 +186,22 @@ __device__ __forceinline__ void ldg_rows2(const int4 *p, int4 &a, int4 &b) {
 #endif
 }
 
+// HJ_CVT_LO: the low int16 half converted as a PRMT sign extension + I2FP
+// (integer ALU) instead of I2F.S16 (the quarter-rate XU pipe).
+#ifndef HJ_CVT_LO
+#define HJ_CVT_LO 0
+#endif
+__device__ __forceinline__ float cvt_lo16(int w) {
+#if HJ_CVT_LO
+    int x;
+    asm("prmt.b32 %0, %1, 0, 0x9910;" : "=r"(x) : "r"(w));
+    float f;
+    asm("cvt.rn.f32.s32 %0, %1;" : "=f"(f) : "r"(x));
+    return f;
+#else
+    return (float)(short)(w & 0xffff);
+#endif
+}
 #ifndef HJ_CVT_H1
 #define HJ_CVT_H1 0
 #endif
@@ -220,7 +236,7 @@ __device__ __forceinline__ bool screen_rows(const int16_t *__restrict__ src, con
         const float q[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
 #pragma unroll
         for (int cp = 0; cp < 4; ++cp) {
-            float c0 = (float)(short)(w[cp] & 0xffff);
+            float c0 = cvt_lo16(w[cp]);
             float c1 = (float)(w[cp] >> 16);
             u64 x = mul2(pk(c0, c1), pk(q[2 * cp], q[2 * cp + 1]));
             X[cp][r] = x;
@@ -331,7 +347,7 @@ __device__ __forceinline__ bool screen_cols(const int16_t *__restrict__ src, con
 #if HJ_CVT_H1
             f[r] = (c & 1) ? (float)(short)((unsigned)w >> 16) : (float)(short)(w & 0xffff);
 #else
-            f[r] = (c & 1) ? (float)(w >> 16) : (float)(short)(w & 0xffff);
+            f[r] = (c & 1) ? (float)(w >> 16) : cvt_lo16(w);
 #endif
         }
         const float4 qa = lds128f(qf + 8 * c), qb = lds128f(qf + 8 * c + 4);
