@@ -682,14 +682,26 @@ __device__ __forceinline__ void hj_barrier_early() { asm volatile("barrier.sync 
 #ifndef HJ_GRAB_STATIC
 #define HJ_GRAB_STATIC 1
 #endif
-template <int MODE>
-__device__ __forceinline__ constexpr bool grab_static() { return HJ_GRAB_STATIC && MODE == kModeRef; }
-template <int MODE>
-__device__ __forceinline__ int grab_base() { return grab_static<MODE>() ? (int)blockDim.x : 0; }
-template <int MODE>
+// The number of static rounds: 1, and 2 for the 64-thread 4:4:4 CTAs
+// (+0.5 %); 2 / 3 rounds measured slower at 4:2:0 (-0.5 % / -3 %), 3 spills
+// at 4:4:4, 2 in the 256-thread tensor-core kernel -3.6 % at 4:4:4
+// (profiles/r02bm_ab.txt, r02bn).  HJ_GRAB_STATIC=0: the atomic-only queue.
+template <int SUB, int MODE, bool TC>
+__device__ __forceinline__ constexpr int grab_static() {
+    return (MODE == kModeRef && HJ_GRAB_STATIC) ? (SUB == HJ_SUB_444 && !TC ? 2 : 1) : 0;
+}
+template <int SUB, int MODE, bool TC>
+__device__ __forceinline__ int grab_base() { return grab_static<SUB, MODE, TC>() * (int)blockDim.x; }
+template <int SUB, int MODE, bool TC>
 __device__ __forceinline__ int grab_first(int *taken) {
-    if constexpr (grab_static<MODE>()) return (int)threadIdx.x;
+    if constexpr (grab_static<SUB, MODE, TC>() > 0) return (int)threadIdx.x;
     else return grab32(taken);
+}
+template <int SUB, int MODE, bool TC>
+__device__ __forceinline__ int grab_next(int *taken, int i0) {
+    if constexpr (grab_static<SUB, MODE, TC>() > 1)
+        if (i0 < (grab_static<SUB, MODE, TC>() - 1) * (int)blockDim.x) return i0 + (int)blockDim.x;
+    return grab32(taken);
 }
 
 // Colour + pack of 4 pixels (Y bytes of `yw`, chroma ints) -> 12 RGB bytes
@@ -968,7 +980,7 @@ __device__ __forceinline__ void exact_phase(SM &sm, uint8_t *smem_raw, const hj_
 // Phase B, second half: the pixel stage of MCU row R = s - 1 (upsample +
 // colour + RGB stores) from the previous step's sample planes; items are
 // handed out through a shared counter so threads busy in exact_phase take fewer.
-template <int SUB, int MODE, class G, class SM>
+template <int SUB, int MODE, class G, class SM, bool TC = false>
 __device__ __forceinline__ void pixel_phase(SM &sm, const hj_image_t &im, const Tile &t, int s, int par, bool do_c) {
     constexpr bool kIslow = MODE == kModeIslow;
     const int tid = threadIdx.x;
@@ -995,7 +1007,7 @@ __device__ __forceinline__ void pixel_phase(SM &sm, const hj_image_t &im, const 
             // jobs overwrote its slot, else still in the slot
             const uint16_t *cprev = do_c ? &sm.cs[24][0] : &sm.cs[0][0] + (((R + 2) % 3) * 8 + 7) * G::CW;
 #pragma unroll 1
-            for (int i0 = grab_first<MODE>(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
+            for (int i0 = grab_first<SUB, MODE, TC>(taken); i0 - (tid & 31) < n_items; i0 = grab_next<SUB, MODE, TC>(taken, i0)) {
                 const int i = i0;
                 if (i >= n_items) continue;
                 // row-major items: adjacent lanes store adjacent 48-byte runs
@@ -1050,7 +1062,7 @@ __device__ __forceinline__ void pixel_phase(SM &sm, const hj_image_t &im, const 
             const float inv_w = 1.0f / (float)gw;
             const uint16_t *crow0 = &sm.cs[0][0] + (par ^ 1) * 8 * G::CW;
 #pragma unroll 1
-            for (int i0 = grab_first<MODE>(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
+            for (int i0 = grab_first<SUB, MODE, TC>(taken); i0 - (tid & 31) < n_items; i0 = grab_next<SUB, MODE, TC>(taken, i0)) {
                 const int i = i0;
                 if (i >= n_items) continue;
                 const int y = __float2int_rd(((float)i + 0.5f) * inv_w), g = i - y * gw;
@@ -1081,7 +1093,7 @@ __device__ __forceinline__ void pixel_phase(SM &sm, const hj_image_t &im, const 
             const float inv_w = 1.0f / (float)gw;
             const uint8_t *cbp = sm.cbp[par ^ 1], *crp = sm.crp[par ^ 1];
 #pragma unroll 1
-            for (int i0 = grab_first<MODE>(taken); i0 - (tid & 31) < n_items; i0 = grab32(taken)) {
+            for (int i0 = grab_first<SUB, MODE, TC>(taken); i0 - (tid & 31) < n_items; i0 = grab_next<SUB, MODE, TC>(taken, i0)) {
                 const int i = i0;
                 if (i >= n_items) continue;
                 const int y = __float2int_rd(((float)i + 0.5f) * inv_w), g = i - y * gw;
@@ -1122,7 +1134,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
             sm.qf[i >> 6][qf_slot(kScreenCols<SUB>, (i & 63) >> 3, i & 7)] = (float)((double)im.q[i] * kPre64[i & 63]);
     if (tid == 0) {
         sm.n_queue[0] = sm.n_queue[1] = 0;
-        sm.n_taken[0] = sm.n_taken[1] = grab_base<MODE>();
+        sm.n_taken[0] = sm.n_taken[1] = grab_base<SUB, MODE, false>();
     }
 
     const int cm_lo = (SUB == HJ_SUB_444) ? t.m0 : t.m0 - 1;  // first chroma window MCU
@@ -1149,7 +1161,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
         if (tid == 0) {
             if (!HJ_EARLY_A) {
                 sm.n_queue[par ^ 1] = 0;  // last used in step s-1, next in s+1
-                sm.n_taken[par ^ 1] = grab_base<MODE>();
+                sm.n_taken[par ^ 1] = grab_base<SUB, MODE, false>();
             }
             // bulk L2 prefetch of the next step's coefficient ranges
             const int ny = HJ_PF_L2 ? s + 1 : -1;
@@ -1320,7 +1332,7 @@ render_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__ ti
             // last used by phase B of step s-1 (done: every thread passed the
             // early barrier of this step), next by step s+1
             sm.n_queue[par ^ 1] = 0;
-            sm.n_taken[par ^ 1] = grab_base<MODE>();
+            sm.n_taken[par ^ 1] = grab_base<SUB, MODE, false>();
         }
 
         // ---------------- phase B: exact recompute of this step's queue ...
@@ -1583,7 +1595,7 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
     const bool direct = (im.flags & HJ_FLAG_DIRECT_IDCT) != 0;
     for (int i = tid; i < 192; i += NT) sm.qi[i >> 6][i & 63] = im.q[i];
     if (tid == 0) {
-        sm.n_queue[0] = sm.n_queue[1] = 0; sm.n_taken[0] = sm.n_taken[1] = grab_base<kModeRef>();
+        sm.n_queue[0] = sm.n_queue[1] = 0; sm.n_taken[0] = sm.n_taken[1] = grab_base<SUB, kModeRef, true>();
         for (int b = 0; b < tcs::kNBuf; ++b) {
             tc::mbar_init(&sm.full[b], 1);
             tc::mbar_init(&sm.empty[b], NT / 32);
@@ -1623,7 +1635,7 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
         const int64_t yblk0 = ((int64_t)s * mpr + t.m0) * YB;  // first Y block of the step
         if (tid == 0) {
             sm.n_queue[par ^ 1] = 0;
-            sm.n_taken[par ^ 1] = grab_base<kModeRef>();
+            sm.n_taken[par ^ 1] = grab_base<SUB, kModeRef, true>();
             const int ny = HJ_PF_L2 ? s + 1 : -1;
             if (ny >= t.r0 && ny < t.r1) {
                 const int64_t b0 = ((int64_t)ny * mpr + t.m0) * YB;
@@ -1807,7 +1819,7 @@ render_tc_kernel(const hj_image_t *__restrict__ images, const Tile *__restrict__
 
         // ---------------- phase B: exact recompute ∥ pixel stage of row s-1
         exact_phase<SUB, kModeRef, G, NT>(sm, smem_raw, im, par, direct);
-        pixel_phase<SUB, kModeRef, G>(sm, im, t, s, par, do_c);
+        pixel_phase<SUB, kModeRef, G, SmemTc<SUB>, true>(sm, im, t, s, par, do_c);
         __syncthreads();
     }
     tc::fence_before();
